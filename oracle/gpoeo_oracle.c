@@ -1,0 +1,501 @@
+/*
+ * gpoeo_oracle.c — plain, slow, obviously-correct CPU oracle for the GPOEO
+ * iteration-period detector (arXiv 2201.01684, Alg. 1 + Alg. 2).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_2201_01684_b200/) never links, imports or calls it, and shares no code,
+ * header, table or constant generator with it.
+ *
+ * Everything is fp64 on the fp32 input bytes, sequential loops in the order the
+ * paper writes them, one trace per call (callers parallelise over traces).
+ * Compiled with -O2 -ffp-contract=off (no FMA contraction).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n. Readings Z1..Z30 are the ones
+ * listed in SURVEY.md 8(c) and DESIGN.md "Readings".
+ *
+ * Steps:
+ *   O1 composite detection signal              P:459 (+ Z1)
+ *   O2 power spectrum by the DFT definition     Alg.1 l.1-2, P:309-310 (+ Z2-Z4)
+ *   O3 peaks -> candidate integer periods       Alg.1 l.3-5, P:311-314 (+ Z5-Z9, Z21)
+ *   O4 Alg. 2 similarity error per candidate    P:353-382 (+ Z10-Z16)
+ *   O5 arg-best candidate                       Alg.1 l.9-10, P:318-319 (+ Z17)
+ *   O6 local range + Alg. 2 on each             Alg.1 l.11-17, P:320-328 (+ Z18, Z19)
+ *   O7 final argmin                             Alg.1 l.18-19, P:329-331 (+ Z17, Z20)
+ *   O8 margins (Z27) and work counters
+ *   O9 exhaustive search (tests only)
+ *
+ * Pins (tests/test_oracle_*.py): O1 closed-form z-scores; O2 numpy.fft.rfft,
+ * Parseval, pure tones, impulse; O3 hand spectra and scipy find_peaks;
+ * CEM: SPEC examples, sklearn KMeans special case, fixed-point
+ * self-consistency; SMAPE values; Alg.2 exact zeros on periodic input;
+ * Alg.1 planted periods and brute force on tiny inputs.
+ * Parity unpinned (a reading, not a paper value): the GMM variant Z12 and the
+ * composite rule Z1 themselves — the paper prints no worked example.
+ */
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_TRACE_OK 0
+#define OR_TRACE_APERIODIC 1
+#define OR_TRACE_INSUFFICIENT 2
+#define OR_TRACE_CONSTANT 3
+
+typedef struct {
+  int32_t n_samples;      /* N                                    */
+  int32_t n_features;     /* F                                    */
+  double sample_interval; /* T_s (scales seconds only, Z25)       */
+  int32_t min_period;     /* L_min (Z21)                          */
+  int32_t max_period;     /* L_max (Z21)                          */
+  double c_peak;          /* c_peak (Z6)                   */
+  int32_t max_candidates; /* K (Z8)                               */
+  int32_t num_groups;     /* NumG (Z12)                           */
+  int32_t gmm_max_iters;  /* CEM cap (Z12)                        */
+  int32_t pad_;
+} or_params;
+
+typedef struct {
+  /* outcome */
+  int32_t status;
+  int32_t period;         /* L*  (-1 if none)                              */
+  double period_s;        /* L* * T_s                                      */
+  double error;           /* Err(L*)                                       */
+  int32_t best_candidate; /* L_b                                           */
+  int32_t best_bin;       /* k_b                                           */
+  int32_t n_candidates;
+  int32_t n_peaks;        /* in-band peaks                                 */
+  int32_t n_passing;      /* peaks above the c_peak threshold              */
+  int32_t cap_binds;      /* 1 if more than K peaks passed (Z8)            */
+  int32_t cand_k[32];
+  int32_t cand_L[32];
+  double cand_P[32];
+  double cand_err[32];
+  int32_t local_lo, local_hi; /* evaluated integer range (after clipping)  */
+  double p_max;
+  /* margins (Z27) */
+  double d_thr, d_peak, d_rank, d_err_cand, d_err_local, d_cem;
+  /* work counters */
+  int64_t n_queries;
+  int64_t samples_clustered; /* sum over queries of (M-1)*L               */
+  int64_t cem_sample_iters;  /* sum over windows of passes*L              */
+} or_result;
+
+/* ------------------------------------------------------------------------ */
+/* O1. Composite detection signal (P:459 names a composite of power, SM util and
+ * mem util; Z1 reading: population z-score per channel, weighted sum, sigma=0
+ * channel contributes 0, y rounded once to fp32). Returns 1 if every channel is
+ * constant. mu/sigma may be NULL. */
+int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, float* y, double* mu_out,
+                     double* sigma_out) {
+  double mu[8], sigma[8];
+  int all_const = 1;
+  for (int c = 0; c < F; ++c) {
+    const float* xc = x + (int64_t)c * N;
+    double s = 0.0;
+    for (int n = 0; n < N; ++n) s += (double)xc[n];
+    mu[c] = s / N;
+    double q = 0.0;
+    for (int n = 0; n < N; ++n) q += ((double)xc[n] - mu[c]) * ((double)xc[n] - mu[c]);
+    sigma[c] = sqrt(q / N);
+    if (sigma[c] > 0.0) all_const = 0;
+    if (mu_out) mu_out[c] = mu[c];
+    if (sigma_out) sigma_out[c] = sigma[c];
+  }
+  for (int n = 0; n < N; ++n) {
+    double v = 0.0;
+    for (int c = 0; c < F; ++c) {
+      if (sigma[c] > 0.0) v += (w ? w[c] : 1.0) * (((double)x[(int64_t)c * N + n] - mu[c]) / sigma[c]);
+    }
+    y[n] = (float)v;
+  }
+  return all_const;
+}
+
+/* ------------------------------------------------------------------------ */
+/* O2. Power spectrum by the definition of the DFT (Alg.1 l.1; Z2: no window,
+ * no padding; Z3/Z4: unnormalised |X_k|^2):
+ *   X_k = sum_{n<N} y[n] (cos(2 pi k n / N) - i sin(2 pi k n / N)),  P_k = |X_k|^2,
+ * k = 0..N/2. The twiddle for (k n mod N) comes from an fp64 table. O(N^2). */
+int oracle_power_spectrum(const float* y, int32_t N, double* P) {
+  double* ct = (double*)malloc(sizeof(double) * N);
+  double* st = (double*)malloc(sizeof(double) * N);
+  if (!ct || !st) { free(ct); free(st); return -1; }
+  for (int m = 0; m < N; ++m) {
+    ct[m] = cos(2.0 * M_PI * (double)m / (double)N);
+    st[m] = sin(2.0 * M_PI * (double)m / (double)N);
+  }
+  for (int k = 0; k <= N / 2; ++k) {
+    double re = 0.0, im = 0.0;
+    for (int n = 0; n < N; ++n) {
+      int64_t m = ((int64_t)k * n) % N;
+      re += (double)y[n] * ct[m];
+      im -= (double)y[n] * st[m];
+    }
+    P[k] = re * re + im * im;
+  }
+  free(ct);
+  free(st);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* SMAPE (Alg.2 l.14; Z14 reading): |a-b| / ((|a|+|b|)/2),
+ * 0 when a = b = 0. */
+double oracle_smape(double a, double b) {
+  double den = (fabs(a) + fabs(b)) / 2.0;
+  if (den == 0.0) return 0.0;
+  return fabs(a - b) / den;
+}
+
+/* ------------------------------------------------------------------------ */
+/* "Gauss(Smp_i, NumG)" (Alg.2 l.8): 1-D Gaussian mixture
+ * clustering. Z12 reading: classification-EM (CEM).
+ *   init: R = max - min; R <= 0 -> one group. Else mu_j = min + (j+1/2) R/G,
+ *         var_j = (R/G)^2, pi_j = 1/G, all alive.
+ *   repeat (at most max_iters assignment passes):
+ *     (1) label_s = argmax_{j alive} [ln pi_j - 1/2 ln var_j - (v_s - mu_j)^2 / (2 var_j)],
+ *         ties -> lowest j;
+ *     (2) stop if no label changed (or the cap is reached);
+ *     (3) per alive j: n_j = |{s: label_s = j}|; n_j = 0 -> dead; else pi_j = n_j / L,
+ *         mu_j = mean, var_j = max(mean (v - mu_j)^2, 1e-6 R^2).
+ * Returns the number of assignment passes; labels[s] in [0, G). If margin != NULL it
+ * receives min over decisions of (s_best - s_second) / (|s_best| + |s_second| + 1). */
+int oracle_gmm_cem(const float* v, int32_t L, int32_t G, int32_t max_iters, uint8_t* labels,
+                   double* margin) {
+  double mn = (double)v[0], mx = (double)v[0];
+  for (int s = 1; s < L; ++s) {
+    if ((double)v[s] < mn) mn = (double)v[s];
+    if ((double)v[s] > mx) mx = (double)v[s];
+  }
+  double R = mx - mn;
+  if (!(R > 0.0) || G == 1) {
+    for (int s = 0; s < L; ++s) labels[s] = 0;
+    return 0;
+  }
+  double mu[8], var[8], pi[8];
+  int alive[8];
+  double w = R / G;
+  for (int j = 0; j < G; ++j) {
+    mu[j] = mn + (j + 0.5) * w;
+    var[j] = w * w;
+    pi[j] = 1.0 / G;
+    alive[j] = 1;
+  }
+  double var_floor = 1e-6 * R * R;
+  uint8_t* prev = (uint8_t*)malloc(L);
+  int it;
+  for (it = 1; it <= max_iters; ++it) {
+    /* (1) assignment */
+    double cj[8];
+    for (int j = 0; j < G; ++j) cj[j] = alive[j] ? (log(pi[j]) - 0.5 * log(var[j])) : 0.0;
+    int changed = 0;
+    for (int s = 0; s < L; ++s) {
+      int best = -1;
+      double sb = 0.0, s2 = -INFINITY, db = 0.0, d2nd = 0.0;
+      for (int j = 0; j < G; ++j) {
+        if (!alive[j]) continue;
+        double d = (double)v[s] - mu[j];
+        double sc = cj[j] - (d * d) / (2.0 * var[j]);
+        if (best < 0 || sc > sb) {
+          if (best >= 0) { s2 = sb; d2nd = db; }
+          best = j;
+          sb = sc;
+          db = d * d;
+        } else if (sc > s2 || (sc == s2 && d * d < d2nd)) {
+          s2 = sc;
+          d2nd = d * d;
+        }
+      }
+      /* Z27 decision margin. At the first pass every component has the same pi and
+       * var, so an exact tie in (v - mu_j)^2 is a structural tie decided by the
+       * "lowest j" rule identically on any implementation: not a margin. */
+      if (margin && s2 > -INFINITY && !(it == 1 && sb == s2 && db == d2nd)) {
+        double m = (sb - s2) / (fabs(sb) + fabs(s2) + 1.0);
+        if (m < *margin) *margin = m;
+      }
+      if (it > 1 && labels[s] != (uint8_t)best) changed = 1;
+      labels[s] = (uint8_t)best;
+    }
+    /* (2) stop */
+    if (it > 1 && !changed) break;
+    if (it == max_iters) break;
+    /* (3) M-step */
+    for (int j = 0; j < G; ++j) {
+      if (!alive[j]) continue;
+      int64_t n = 0;
+      double s1 = 0.0;
+      for (int s = 0; s < L; ++s)
+        if (labels[s] == j) { ++n; s1 += (double)v[s]; }
+      if (n == 0) { alive[j] = 0; continue; }
+      mu[j] = s1 / (double)n;
+      double q = 0.0;
+      for (int s = 0; s < L; ++s)
+        if (labels[s] == j) q += ((double)v[s] - mu[j]) * ((double)v[s] - mu[j]);
+      var[j] = q / (double)n;
+      if (var[j] < var_floor) var[j] = var_floor;
+      pi[j] = (double)n / (double)L;
+    }
+    memcpy(prev, labels, L);
+  }
+  free(prev);
+  return it > max_iters ? max_iters : it;
+}
+
+static double mean_of(const float* v, int32_t L) {
+  double s = 0.0;
+  for (int i = 0; i < L; ++i) s += (double)v[i];
+  return s / L;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Alg. 2, feature sequence similarity, for integer window length L
+ * (Num_s = floor(T/T_s) = L, Z11) over M = floor(N/L) whole windows (Z10):
+ *   for i = 1..M-1:  Mean_prev = mean(Smp_i); Mean_back = mean(Smp_{i+1});
+ *     GaGrp = Gauss(Smp_i, NumG);
+ *     for each group j: RelValPrev_j = mean(Smp_i[GaGrp_j]) - Mean_prev,
+ *                       RelValBack_j = mean(Smp_{i+1}[GaGrp_j]) - Mean_back,
+ *                       grperr_j = SMAPE(RelValPrev_j, RelValBack_j);
+ *     err_i = sum_j |GaGrp_j| grperr_j / sum_j |GaGrp_j|
+ *   Err_T = mean_i err_i.
+ * Returns -1 if M < 2. Counters may be NULL. */
+double oracle_similarity_error(const float* y, int32_t N, int32_t L, int32_t G, int32_t max_iters,
+                               double* cem_margin, int64_t* cem_sample_iters) {
+  int32_t M = N / L;
+  if (L < 1 || M < 2) return -1.0;
+  uint8_t* lab = (uint8_t*)malloc(L);
+  float* gp = (float*)malloc(sizeof(float) * L);
+  float* gb = (float*)malloc(sizeof(float) * L);
+  double err_sum = 0.0;
+  for (int i = 0; i < M - 1; ++i) {
+    const float* prev = y + (int64_t)i * L;
+    const float* back = y + (int64_t)(i + 1) * L;
+    double mean_prev = mean_of(prev, L);
+    double mean_back = mean_of(back, L);
+    int passes = oracle_gmm_cem(prev, L, G, max_iters, lab, cem_margin);
+    if (cem_sample_iters) *cem_sample_iters += (int64_t)(passes > 0 ? passes : 1) * L;
+    double num = 0.0, den = 0.0;
+    for (int j = 0; j < G; ++j) {
+      int n = 0;
+      for (int s = 0; s < L; ++s)
+        if (lab[s] == j) { gp[n] = prev[s]; gb[n] = back[s]; ++n; }
+      if (n == 0) continue;
+      double rel_prev = mean_of(gp, n) - mean_prev;
+      double rel_back = mean_of(gb, n) - mean_back;
+      num += (double)n * oracle_smape(rel_prev, rel_back);
+      den += (double)n;
+    }
+    err_sum += num / den;
+  }
+  free(lab);
+  free(gp);
+  free(gb);
+  return err_sum / (M - 1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* O3 helpers */
+static double mirrored(const double* P, int32_t N, int64_t k) {
+  /* P[-k] = P[k], P[N/2 + d] = P[N/2 - d] (real-input spectrum symmetry) */
+  if (k < 0) k = -k;
+  if (k > N / 2) k = N - k;
+  return P[k];
+}
+
+/* Band of bins whose integer period floor(N/k) lies in [L_min, L_max] (Z9, Z21). */
+static int in_band(int32_t N, int64_t k, int32_t Lmin, int32_t Lmax) {
+  if (k < 1) return 0;
+  int64_t Lk = (int64_t)N / k;
+  return Lk >= Lmin && Lk <= Lmax;
+}
+
+/* Candidate selection (Alg.1 l.3-5; Z5 peak definition, Z7 in-band
+ * max, Z8 top-K then threshold, Z9 integer mapping, dedupe keeps the first in
+ * (P desc, k asc) order). Fills r->cand_*, r->n_candidates, margins d_thr,
+ * d_peak, d_rank, p_max. Returns number of candidates. */
+int oracle_candidates(const double* P, const or_params* p, or_result* r) {
+  const int32_t N = p->n_samples;
+  const int32_t K = p->max_candidates;
+  const double c = p->c_peak;
+  int32_t npk = 0;
+  int32_t* pk = (int32_t*)malloc(sizeof(int32_t) * (N / 2 + 1));
+  for (int64_t k = 1; k <= N / 2; ++k) {
+    if (!in_band(N, k, p->min_period, p->max_period)) continue;
+    if (P[k] > mirrored(P, N, k - 1) && P[k] >= mirrored(P, N, k + 1)) pk[npk++] = (int32_t)k;
+  }
+  r->n_peaks = npk;
+  r->n_candidates = 0;
+  r->n_passing = 0;
+  r->cap_binds = 0;
+  r->p_max = 0.0;
+  r->d_thr = r->d_peak = r->d_rank = INFINITY;
+  if (npk == 0) { free(pk); return 0; }
+  /* rank by (P desc, k asc): simple insertion sort */
+  for (int i = 1; i < npk; ++i) {
+    int32_t v = pk[i];
+    int j = i - 1;
+    while (j >= 0 && (P[pk[j]] < P[v] || (P[pk[j]] == P[v] && pk[j] > v))) { pk[j + 1] = pk[j]; --j; }
+    pk[j + 1] = v;
+  }
+  double pmax = P[pk[0]];
+  double thr = c * c * pmax;
+  r->p_max = pmax;
+  int passing = 0;
+  for (int i = 0; i < npk; ++i)
+    if (P[pk[i]] > thr) ++passing;
+  r->n_passing = passing;
+  r->cap_binds = passing > K;
+  /* margins (Z27), relative to P_max */
+  for (int i = 0; i < npk; ++i) {
+    double m = fabs(P[pk[i]] - thr) / pmax;
+    if (m < r->d_thr) r->d_thr = m;
+  }
+  for (int64_t k = 1; k <= N / 2; ++k) {
+    if (!in_band(N, k, p->min_period, p->max_period)) continue;
+    if (P[k] < thr * (1.0 - 1e-3)) continue; /* only bins that could become candidates */
+    double m1 = fabs(P[k] - mirrored(P, N, k - 1)) / pmax;
+    double m2 = fabs(P[k] - mirrored(P, N, k + 1)) / pmax;
+    if (m1 < r->d_peak) r->d_peak = m1;
+    if (m2 < r->d_peak) r->d_peak = m2;
+  }
+  if (passing > K) r->d_rank = fabs(P[pk[K - 1]] - P[pk[K]]) / pmax;
+  /* top-K, threshold, integer period, dedupe */
+  int nc = 0;
+  for (int i = 0; i < npk && i < K; ++i) {
+    int32_t k = pk[i];
+    if (!(P[k] > thr)) break;
+    int32_t Lk = N / k;
+    int dup = 0;
+    for (int q = 0; q < nc; ++q)
+      if (r->cand_L[q] == Lk) dup = 1;
+    if (dup) continue;
+    r->cand_k[nc] = k;
+    r->cand_L[nc] = Lk;
+    r->cand_P[nc] = P[k];
+    ++nc;
+  }
+  r->n_candidates = nc;
+  free(pk);
+  return nc;
+}
+
+/* Z18: local range around the fractional centre Tc = N/k_b (Z19), in samples:
+ *   N_T = (N-1)/Tc,  T_low = Tc (1 - 1/(N_T+1)) = N(N-1)/((N-1)k_b + N),
+ *   T_up = Tc (1 + 1/(N_T-1)) = N(N-1)/((N-1)k_b - N),
+ * evaluated set = integers floor(T_low)..floor(T_up), clipped. */
+void oracle_local_range(int32_t N, int32_t k_b, int32_t Lmin, int32_t Lmax, int32_t* lo, int32_t* hi) {
+  int64_t num = (int64_t)N * (N - 1);
+  int64_t l = num / ((int64_t)(N - 1) * k_b + N);
+  int64_t h = num / ((int64_t)(N - 1) * k_b - N);
+  if (l < Lmin) l = Lmin;
+  if (h > Lmax) h = Lmax;
+  *lo = (int32_t)l;
+  *hi = (int32_t)h;
+}
+
+static double rel_gap(double best, double second) {
+  if (second == best) return (best == 0.0) ? INFINITY : 0.0; /* exact zeros tie reproducibly (Z28) */
+  return (second - best) / (best > 1e-12 ? best : 1e-12);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Alg. 1 on one trace x[F][N]. local_err (optional) receives Err for each L in
+ * [local_lo, local_hi]; size >= L_max - L_min + 1. */
+int oracle_detect(const float* x, const or_params* p, const double* weights, or_result* r, double* local_err) {
+  memset(r, 0, sizeof(*r));
+  const int32_t N = p->n_samples;
+  if (N < 8 || p->n_features < 1 || p->n_features > 8 || p->min_period < 2 || p->max_period < p->min_period ||
+      p->max_period > N / 2 || p->max_candidates < 1 || p->max_candidates > 32 || p->num_groups < 1 ||
+      p->num_groups > 8 || p->gmm_max_iters < 1 || !(p->c_peak > 0.0) || p->c_peak > 1.0)
+    return -1;
+  r->period = -1;
+  r->best_candidate = -1;
+  r->best_bin = -1;
+  r->d_thr = r->d_peak = r->d_rank = r->d_err_cand = r->d_err_local = r->d_cem = INFINITY;
+  float* y = (float*)malloc(sizeof(float) * N);
+  double* P = (double*)malloc(sizeof(double) * (N / 2 + 1));
+  /* O1 */
+  int constant = oracle_composite(x, N, p->n_features, weights, y, NULL, NULL);
+  if (constant) { r->status = OR_TRACE_CONSTANT; goto done; }
+  {
+    /* band must be non-empty and hold >= 2 windows (Z21) */
+    int any = 0;
+    for (int64_t k = 1; k <= N / 2; ++k) any |= in_band(N, k, p->min_period, p->max_period);
+    if (!any || N < 2 * p->min_period) { r->status = OR_TRACE_INSUFFICIENT; goto done; }
+  }
+  /* O2 */
+  oracle_power_spectrum(y, N, P);
+  /* O3 */
+  if (oracle_candidates(P, p, r) == 0) { r->status = OR_TRACE_APERIODIC; goto done; }
+  /* O4 + O5 */
+  int best = -1;
+  for (int q = 0; q < r->n_candidates; ++q) {
+    double e = oracle_similarity_error(y, N, r->cand_L[q], p->num_groups, p->gmm_max_iters, &r->d_cem,
+                                       &r->cem_sample_iters);
+    r->cand_err[q] = e;
+    r->n_queries++;
+    r->samples_clustered += (int64_t)(N / r->cand_L[q] - 1) * r->cand_L[q];
+    if (best < 0 || e < r->cand_err[best] || (e == r->cand_err[best] && r->cand_L[q] < r->cand_L[best])) best = q;
+  }
+  {
+    double second = INFINITY;
+    for (int q = 0; q < r->n_candidates; ++q)
+      if (q != best && r->cand_err[q] < second) second = r->cand_err[q];
+    r->d_err_cand = rel_gap(r->cand_err[best], second);
+  }
+  r->best_candidate = r->cand_L[best];
+  r->best_bin = r->cand_k[best];
+  /* O6 */
+  int32_t lo, hi;
+  oracle_local_range(N, r->best_bin, p->min_period, p->max_period, &lo, &hi);
+  r->local_lo = lo;
+  r->local_hi = hi;
+  /* O7 */
+  double* le = local_err ? local_err : (double*)malloc(sizeof(double) * (hi - lo + 1));
+  for (int32_t L = lo; L <= hi; ++L) {
+    double e = -1.0;
+    for (int q = 0; q < r->n_candidates; ++q)
+      if (r->cand_L[q] == L) e = r->cand_err[q]; /* memoised: the same Alg.2 value */
+    if (e < 0.0) {
+      e = oracle_similarity_error(y, N, L, p->num_groups, p->gmm_max_iters, &r->d_cem, &r->cem_sample_iters);
+      r->n_queries++;
+      r->samples_clustered += (int64_t)(N / L - 1) * L;
+    }
+    le[L - lo] = e;
+  }
+  int32_t Lbest = lo;
+  for (int32_t L = lo + 1; L <= hi; ++L)
+    if (le[L - lo] < le[Lbest - lo]) Lbest = L; /* strict: ties keep the smaller L (Z17) */
+  double ebest = le[Lbest - lo], esecond = INFINITY;
+  for (int32_t L = lo; L <= hi; ++L)
+    if (L != Lbest && le[L - lo] < esecond) esecond = le[L - lo];
+  if (!local_err) free(le);
+  r->d_err_local = rel_gap(ebest, esecond);
+  r->period = Lbest;
+  r->period_s = (double)Lbest * p->sample_interval;
+  r->error = ebest;
+  r->status = OR_TRACE_OK;
+done:
+  free(y);
+  free(P);
+  return 0;
+}
+
+/* O9 (tests only): Err(L) for every L in [L_min, L_max] of an already-formed
+ * signal y; returns the global argmin (Err, L). */
+int32_t oracle_exhaustive(const float* y, int32_t N, int32_t Lmin, int32_t Lmax, int32_t G, int32_t max_iters,
+                          double* errs) {
+  int32_t best = -1;
+  double eb = 0.0;
+  for (int32_t L = Lmin; L <= Lmax; ++L) {
+    double e = oracle_similarity_error(y, N, L, G, max_iters, NULL, NULL);
+    if (errs) errs[L - Lmin] = e;
+    if (best < 0 || e < eb) { best = L; eb = e; }
+  }
+  return best;
+}
+
+int oracle_sizeof_params(void) { return (int)sizeof(or_params); }
+int oracle_sizeof_result(void) { return (int)sizeof(or_result); }
