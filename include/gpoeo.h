@@ -1,0 +1,169 @@
+/*
+ * gpoeo.h — C ABI of libgpoeo.so, the B200 (sm_100a) batched implementation of the
+ * GPOEO iteration-period detector (arXiv 2201.01684): Alg. 1 "Period calculation
+ * based on FFT and feature sequence similarity" with Alg. 2
+ * "Feature sequence similarity", over a batch of telemetry traces.
+ *
+ * Citations: P:n = PAPER.md line n. Readings Z1..Z30 = DESIGN.md "Readings" (the
+ * places the paper is silent or garbled and the interpretation this library fixes).
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless a comment says HOST.
+ *  - The caller owns every buffer (traces, results, workspace). The library never
+ *    allocates device memory, never frees, and never synchronises the stream in the
+ *    device-pointer entry points: they only enqueue kernels on `stream` (cudaStream_t
+ *    passed as void*; NULL = legacy default stream) and return.
+ *  - Argument errors are detected synchronously, before any launch, and returned as a
+ *    negative gpoeo_status; nothing is enqueued then. A launch failure returns
+ *    GPOEO_ERR_CUDA. Per-trace outcomes (aperiodic, constant, ...) never fail a call:
+ *    they are reported in gpoeo_result.status.
+ *  - Reentrant: no global mutable state. Two calls may run concurrently on different
+ *    streams with different workspaces.
+ *  - There is no CPU fallback: without a usable CUDA device every compute entry point
+ *    returns GPOEO_ERR_CUDA.
+ */
+#ifndef GPOEO_H
+#define GPOEO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPOEO_API_VERSION 1
+#define GPOEO_MAX_FEATURES 8
+#define GPOEO_MAX_CANDIDATES 32
+#define GPOEO_MAX_GROUPS 8
+#define GPOEO_MIN_LOG2N 3
+#define GPOEO_MAX_LOG2N 18
+
+typedef enum {
+  GPOEO_OK = 0,
+  GPOEO_ERR_INVALID_ARGUMENT = -1, /* a parameter is out of range or a pointer is NULL   */
+  GPOEO_ERR_UNSUPPORTED = -2,      /* N not a power of two in [2^3, 2^18]                */
+  GPOEO_ERR_WORKSPACE = -3,        /* workspace NULL or smaller than gpoeo_workspace_size */
+  GPOEO_ERR_MISALIGNED = -4,       /* traces/workspace not 16-B aligned, stride % 4 != 0  */
+  GPOEO_ERR_CUDA = -5              /* no device / launch failure                          */
+} gpoeo_status;
+
+typedef enum {
+  GPOEO_TRACE_OK = 0,           /* period found                                             */
+  GPOEO_TRACE_APERIODIC = 1,    /* no in-band spectral peak -> no candidate (Z22)    */
+  GPOEO_TRACE_INSUFFICIENT = 2, /* no bin k with L_min <= floor(N/k) <= L_max (Z21)         */
+  GPOEO_TRACE_CONSTANT = 3      /* every feature channel has zero variance (Z1)             */
+} gpoeo_trace_status;
+
+/* Parameters of Alg. 1/2 for one call (every trace of the batch shares them). */
+typedef struct {
+  int32_t n_samples;      /* N, samples per trace: power of two, 2^3..2^18                  */
+  int32_t n_features;     /* F, feature channels per trace (power, SM util, mem util: P:459),
+                             1..8                                                            */
+  int64_t trace_stride;   /* floats between consecutive traces, >= F*N, multiple of 4       */
+  double sample_interval; /* T_s [s] > 0. Labels frequencies only (Alg.1 l.1); it never
+                             changes the detected integer period (Z25), only period_s       */
+  int32_t min_period;     /* L_min >= 2 samples (candidate band, Z21)                       */
+  int32_t max_period;     /* L_max, L_min <= L_max <= N/2 (>= 2 windows, Alg.2 l.1)         */
+  float c_peak;           /* c_peak in (0, 1], default 0.65 ("0.6-0.7", Z6)           */
+  int32_t max_candidates; /* K in [1, 32], default 16: top-K peaks kept (Z8)                */
+  int32_t num_groups;     /* NumG in [1, 8], default 4: GMM groups of Alg.2 l.8 (Z12)       */
+  int32_t gmm_max_iters;  /* >= 1, default 32: CEM assignment-pass cap (Z12)                */
+  float feature_weights[GPOEO_MAX_FEATURES]; /* w_c of the composite (Z1), default 1     */
+} gpoeo_params;
+
+/* Per-trace result of Alg. 1. 24 bytes. */
+typedef struct {
+  int32_t period;         /* T_iter as an integer number of samples L* (Z20); -1 if none    */
+  float period_s;         /* L* * T_s [s]                                                   */
+  float error;            /* err = Err(L*) of Alg. 2, rounded to fp32 (Z23)                 */
+  int32_t status;         /* gpoeo_trace_status                                             */
+  int32_t best_candidate; /* L_b = floor(N / k_b), best FFT candidate (Alg.1 l.9-10)        */
+  int32_t n_candidates;   /* |TCand| after top-K, threshold and dedupe (Alg.1 l.4-5)        */
+} gpoeo_result;
+
+/* Optional per-trace detail (debug/parity surface of gpoeo_detect_periods_ex). */
+typedef struct {
+  int32_t n_candidates;
+  int32_t best_bin;      /* k_b                                                              */
+  int32_t local_lo;      /* evaluated local range [local_lo, local_hi] (Alg.1 l.11-13, Z18) */
+  int32_t local_hi;
+  int32_t cand_k[GPOEO_MAX_CANDIDATES];     /* spectral bin of each candidate               */
+  int32_t cand_L[GPOEO_MAX_CANDIDATES];     /* integer period floor(N/k)                    */
+  float cand_P[GPOEO_MAX_CANDIDATES];       /* |X_k|^2                                      */
+  double cand_err[GPOEO_MAX_CANDIDATES];    /* Err(L) of Alg. 2, fp64                       */
+  double best_err;                          /* Err(L*), fp64                                */
+} gpoeo_detail;
+
+/* Fill *p with the defaults above for (N, F, T_s): L_min = 2, L_max = N/2, c_peak 0.65,
+ * K 16, NumG 4, CEM cap 32, weights 1, trace_stride = F*N rounded up to 4. HOST call. */
+void gpoeo_default_params(gpoeo_params* p, int32_t n_samples, int32_t n_features, double sample_interval);
+
+/* Validate *p (HOST). Returns GPOEO_OK or the error code the compute calls would return. */
+int gpoeo_validate_params(const gpoeo_params* p);
+
+/* Workspace bytes gpoeo_detect_periods needs for `batch` traces with *p (HOST, pure).
+ * Returns 0 if *p is invalid. Layout: the composite signal
+ * y[B][N] fp32, candidate lists, the local-search work list and scores, counters. */
+size_t gpoeo_workspace_size(const gpoeo_params* p, int64_t batch);
+
+/* Alg. 1 over a batch (the north-star entry point).
+ *  traces    [batch][trace_stride] fp32, feature-major per trace: x[b][c][n] at
+ *            traces[b*trace_stride + c*N + n]; 16-B aligned.
+ *  results   [batch] gpoeo_result, written once per trace.
+ *  workspace >= gpoeo_workspace_size(p, batch) bytes, 256-B aligned recommended (16-B
+ *            required); contents are scratch (no state carried between calls).
+ *  stream    cudaStream_t (void*). Asynchronous: returns after enqueueing. */
+int gpoeo_detect_periods(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same, plus optional per-trace detail (device array [batch], may be NULL) and optional
+ * device copy of the composite signal left in the workspace (see gpoeo_signal_offset). */
+int gpoeo_detect_periods_ex(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
+                            gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream);
+
+/* End-to-end variant over HOST buffers (the e2e path of bench.py):
+ *  host_traces  HOST [batch][trace_stride] fp32 (pinned memory gives async overlap);
+ *  host_results HOST [batch] gpoeo_result.
+ * Streams chunks of `chunk` traces through the workspace (size it with
+ * gpoeo_workspace_size_host), overlapping H2D copies with compute on an internal copy
+ * stream, and SYNCHRONISES `stream` before returning (results are on the host). */
+size_t gpoeo_workspace_size_host(const gpoeo_params* p, int64_t chunk);
+int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpoeo_params* p,
+                              gpoeo_result* host_results, int64_t chunk, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* Debug/parity surface mirroring fft_spectrum: composite signal (Z1) and its
+ * unnormalised power spectrum P[k] = |X_k|^2, k = 0..N/2 (Alg.1 l.1-2, Z2-Z4).
+ *  spectra [batch][N/2+1] fp32 (may be NULL), signal [batch][N] fp32 (may be NULL).
+ * Same workspace rules as gpoeo_detect_periods. */
+int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params* p, float* spectra, float* signal,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Debug/parity surface mirroring sequence_similarity_error: Alg. 2 Err(L) for
+ * n_queries (trace_index[q], period[q]) pairs on an already-formed signal[batch][N]
+ * (fp32, contiguous rows). error_out [n_queries] fp64. Requires 2 <= period <= N/2.
+ * Workspace: gpoeo_similarity_workspace_size(n_queries) bytes. */
+size_t gpoeo_similarity_workspace_size(int64_t n_queries);
+int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples, const int32_t* trace_index,
+                           const int32_t* period, int64_t n_queries, int32_t num_groups, int32_t gmm_max_iters,
+                           double* error_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Work counters of the last device-pointer call that used `workspace` (HOST read after
+ * the caller synchronised): number of Alg.2 queries and CEM sample-passes. Used by
+ * bench.py to report ALU roofline numbers. Returns GPOEO_OK. */
+typedef struct {
+  int64_t n_candidate_queries;
+  int64_t n_local_queries;
+  int64_t cem_sample_passes; /* sum over windows of (CEM passes x L) + final pass over W_{i+1} */
+} gpoeo_counters;
+int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t batch, gpoeo_counters* out,
+                        void* stream);
+
+const char* gpoeo_status_string(int status);
+int gpoeo_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPOEO_H */

@@ -86,11 +86,14 @@ typedef struct {
 /* ------------------------------------------------------------------------ */
 /* O1. Composite detection signal (P:459 names a composite of power, SM util and
  * mem util; Z1 reading: population z-score per channel, weighted sum, sigma=0
- * channel contributes 0, y rounded once to fp32). Returns 1 if every channel is
- * constant. mu/sigma may be NULL. */
+ * channel contributes 0, y rounded once to fp32):
+ *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N),
+ *   y[n] = fp32( sum_c a_c (x_c[n] - mu_c) ),  a_c = w_c / sigma_c  (Z23: the scale
+ *   a_c is formed once per channel, products and sums in channel order, no FMA).
+ * Returns 1 if every channel is constant. mu/sigma may be NULL. */
 int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, float* y, double* mu_out,
                      double* sigma_out) {
-  double mu[8], sigma[8];
+  double mu[8], sigma[8], a[8];
   int all_const = 1;
   for (int c = 0; c < F; ++c) {
     const float* xc = x + (int64_t)c * N;
@@ -100,6 +103,7 @@ int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, floa
     double q = 0.0;
     for (int n = 0; n < N; ++n) q += ((double)xc[n] - mu[c]) * ((double)xc[n] - mu[c]);
     sigma[c] = sqrt(q / N);
+    a[c] = sigma[c] > 0.0 ? (w ? w[c] : 1.0) / sigma[c] : 0.0;
     if (sigma[c] > 0.0) all_const = 0;
     if (mu_out) mu_out[c] = mu[c];
     if (sigma_out) sigma_out[c] = sigma[c];
@@ -107,7 +111,7 @@ int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, floa
   for (int n = 0; n < N; ++n) {
     double v = 0.0;
     for (int c = 0; c < F; ++c) {
-      if (sigma[c] > 0.0) v += (w ? w[c] : 1.0) * (((double)x[(int64_t)c * N + n] - mu[c]) / sigma[c]);
+      if (sigma[c] > 0.0) v += a[c] * ((double)x[(int64_t)c * N + n] - mu[c]);
     }
     y[n] = (float)v;
   }
