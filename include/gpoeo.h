@@ -31,6 +31,9 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
 
 #define GPOEO_API_VERSION 1
 #define GPOEO_MAX_FEATURES 8
@@ -163,6 +166,9 @@ int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t ba
 const char* gpoeo_status_string(int status);
 int gpoeo_version(void);
 
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

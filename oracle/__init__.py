@@ -38,7 +38,7 @@ class OrParams(ctypes.Structure):
         ("max_candidates", ctypes.c_int32),
         ("num_groups", ctypes.c_int32),
         ("gmm_max_iters", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("dft_band_only", ctypes.c_int32),
     ]
 
 
@@ -92,6 +92,8 @@ def _L():
         lib.oracle_composite.restype = ctypes.c_int
         lib.oracle_power_spectrum.argtypes = [P, ctypes.c_int32, P]
         lib.oracle_power_spectrum.restype = ctypes.c_int
+        lib.oracle_power_spectrum_range.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P]
+        lib.oracle_power_spectrum_range.restype = ctypes.c_int
         lib.oracle_smape.argtypes = [ctypes.c_double, ctypes.c_double]
         lib.oracle_smape.restype = ctypes.c_double
         lib.oracle_gmm_cem.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P]
@@ -131,6 +133,7 @@ class Params:
     num_groups: int = 4
     gmm_max_iters: int = 32
     weights: tuple | None = None
+    dft_band_only: bool = False
 
     def c(self) -> OrParams:
         p = OrParams()
@@ -144,6 +147,7 @@ class Params:
         p.max_candidates = self.max_candidates
         p.num_groups = self.num_groups
         p.gmm_max_iters = self.gmm_max_iters
+        p.dft_band_only = int(self.dft_band_only)
         return p
 
 
@@ -172,6 +176,15 @@ def power_spectrum(y: np.ndarray) -> np.ndarray:
     if _L().oracle_power_spectrum(_ptr(y), y.size, _ptr(P)) != 0:
         raise MemoryError
     return P
+
+
+def power_spectrum_bins(y: np.ndarray, k0: int, k1: int) -> np.ndarray:
+    """O2 at bins k0..k1 only (same arithmetic per bin); returns P[k0..k1]."""
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    P = np.full(y.size // 2 + 1, np.nan)
+    if _L().oracle_power_spectrum_range(_ptr(y), y.size, k0, k1, _ptr(P)) != 0:
+        raise MemoryError
+    return P[k0:k1 + 1].copy()
 
 
 def smape(a: float, b: float) -> float:
@@ -245,7 +258,8 @@ def detect(x: np.ndarray, params: Params) -> Detection:
     p = params.c()
     r = OrResult()
     le = np.full(max(1, p.max_period - p.min_period + 1), np.nan)
-    w = None if params.weights is None else np.ascontiguousarray(params.weights, dtype=np.float64)
+    # the ABI carries w_c as fp32: use the same values
+    w = None if params.weights is None else np.asarray(params.weights, np.float32).astype(np.float64)
     rc = _L().oracle_detect(_ptr(x), ctypes.byref(p), None if w is None else _ptr(w), ctypes.byref(r), _ptr(le))
     if rc != 0:
         raise ValueError("oracle_detect: invalid parameters")

@@ -54,7 +54,8 @@ typedef struct {
   int32_t max_candidates; /* K (Z8)                               */
   int32_t num_groups;     /* NumG (Z12)                           */
   int32_t gmm_max_iters;  /* CEM cap (Z12)                        */
-  int32_t pad_;
+  int32_t dft_band_only;  /* 1: evaluate the DFT only at the bins O3 reads (the band and
+                             its two neighbours); other P[k] are left NaN. Same values. */
 } or_params;
 
 typedef struct {
@@ -123,7 +124,7 @@ int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, floa
  * no padding; Z3/Z4: unnormalised |X_k|^2):
  *   X_k = sum_{n<N} y[n] (cos(2 pi k n / N) - i sin(2 pi k n / N)),  P_k = |X_k|^2,
  * k = 0..N/2. The twiddle for (k n mod N) comes from an fp64 table. O(N^2). */
-int oracle_power_spectrum(const float* y, int32_t N, double* P) {
+int oracle_power_spectrum_range(const float* y, int32_t N, int32_t k0, int32_t k1, double* P) {
   double* ct = (double*)malloc(sizeof(double) * N);
   double* st = (double*)malloc(sizeof(double) * N);
   if (!ct || !st) { free(ct); free(st); return -1; }
@@ -131,7 +132,7 @@ int oracle_power_spectrum(const float* y, int32_t N, double* P) {
     ct[m] = cos(2.0 * M_PI * (double)m / (double)N);
     st[m] = sin(2.0 * M_PI * (double)m / (double)N);
   }
-  for (int k = 0; k <= N / 2; ++k) {
+  for (int k = k0; k <= k1; ++k) {
     double re = 0.0, im = 0.0;
     for (int n = 0; n < N; ++n) {
       int64_t m = ((int64_t)k * n) % N;
@@ -143,6 +144,10 @@ int oracle_power_spectrum(const float* y, int32_t N, double* P) {
   free(ct);
   free(st);
   return 0;
+}
+
+int oracle_power_spectrum(const float* y, int32_t N, double* P) {
+  return oracle_power_spectrum_range(y, N, 0, N / 2, P);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -430,7 +435,21 @@ int oracle_detect(const float* x, const or_params* p, const double* weights, or_
     if (!any || N < 2 * p->min_period) { r->status = OR_TRACE_INSUFFICIENT; goto done; }
   }
   /* O2 */
-  oracle_power_spectrum(y, N, P);
+  if (p->dft_band_only) {
+    int32_t k0 = N, k1 = 0;
+    for (int64_t k = 1; k <= N / 2; ++k)
+      if (in_band(N, k, p->min_period, p->max_period)) {
+        if (k < k0) k0 = (int32_t)k;
+        if (k > k1) k1 = (int32_t)k;
+      }
+    for (int k = 0; k <= N / 2; ++k) P[k] = NAN;
+    k0 = k0 - 1 < 0 ? 0 : k0 - 1;
+    k1 = k1 + 1 > N / 2 ? N / 2 : k1 + 1;
+    oracle_power_spectrum_range(y, N, k0, k1, P);
+    if (k1 == N / 2 && N / 2 - 1 < k0) oracle_power_spectrum_range(y, N, N / 2 - 1, N / 2 - 1, P);
+  } else {
+    oracle_power_spectrum(y, N, P);
+  }
   /* O3 */
   if (oracle_candidates(P, p, r) == 0) { r->status = OR_TRACE_APERIODIC; goto done; }
   /* O4 + O5 */

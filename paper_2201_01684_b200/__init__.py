@@ -1,0 +1,257 @@
+"""Python binding of libgpoeo.so — the B200 GPOEO iteration-period detector.
+
+Argument marshalling only: every step of Alg. 1 / Alg. 2 runs in
+the CUDA kernels behind the C ABI declared in include/gpoeo.h. PyTorch supplies device
+memory and streams. There is no CPU fallback: if the library cannot be built or loaded,
+or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+MAX_FEATURES = 8
+MAX_CANDIDATES = 32
+
+TRACE_OK, TRACE_APERIODIC, TRACE_INSUFFICIENT, TRACE_CONSTANT = 0, 1, 2, 3
+STATUS_NAMES = {0: "ok", 1: "aperiodic", 2: "insufficient", 3: "constant"}
+
+
+class GpoeoParams(ctypes.Structure):
+    _fields_ = [
+        ("n_samples", ctypes.c_int32),
+        ("n_features", ctypes.c_int32),
+        ("trace_stride", ctypes.c_int64),
+        ("sample_interval", ctypes.c_double),
+        ("min_period", ctypes.c_int32),
+        ("max_period", ctypes.c_int32),
+        ("c_peak", ctypes.c_float),
+        ("max_candidates", ctypes.c_int32),
+        ("num_groups", ctypes.c_int32),
+        ("gmm_max_iters", ctypes.c_int32),
+        ("feature_weights", ctypes.c_float * MAX_FEATURES),
+    ]
+
+
+class GpoeoCounters(ctypes.Structure):
+    _fields_ = [("n_candidate_queries", ctypes.c_int64), ("n_local_queries", ctypes.c_int64),
+                ("cem_sample_passes", ctypes.c_int64)]
+
+
+RESULT_DTYPE = np.dtype([("period", "<i4"), ("period_s", "<f4"), ("error", "<f4"), ("status", "<i4"),
+                         ("best_candidate", "<i4"), ("n_candidates", "<i4")])
+DETAIL_DTYPE = np.dtype([("n_candidates", "<i4"), ("best_bin", "<i4"), ("local_lo", "<i4"), ("local_hi", "<i4"),
+                         ("cand_k", "<i4", (MAX_CANDIDATES,)), ("cand_L", "<i4", (MAX_CANDIDATES,)),
+                         ("cand_P", "<f4", (MAX_CANDIDATES,)), ("cand_err", "<f8", (MAX_CANDIDATES,)),
+                         ("best_err", "<f8")])
+assert RESULT_DTYPE.itemsize == 24 and DETAIL_DTYPE.itemsize == 664
+
+_lib = None
+
+
+class GpoeoError(RuntimeError):
+    pass
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load():
+    """Build (if stale) and load libgpoeo.so. Raises if that is impossible."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    try:
+        _build.build()
+    except Exception as e:  # nvcc missing on a run box: use the shipped .so if present
+        if not os.path.exists(path):
+            raise GpoeoError(f"libgpoeo.so is missing and cannot be built: {e}") from e
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    PP = ctypes.POINTER(GpoeoParams)
+    lib.gpoeo_default_params.argtypes = [PP, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
+    lib.gpoeo_default_params.restype = None
+    lib.gpoeo_validate_params.argtypes = [PP]
+    lib.gpoeo_validate_params.restype = ctypes.c_int
+    lib.gpoeo_workspace_size.argtypes = [PP, ctypes.c_int64]
+    lib.gpoeo_workspace_size.restype = ctypes.c_size_t
+    lib.gpoeo_detect_periods.argtypes = [P, ctypes.c_int64, PP, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_detect_periods.restype = ctypes.c_int
+    lib.gpoeo_detect_periods_ex.argtypes = [P, ctypes.c_int64, PP, P, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_detect_periods_ex.restype = ctypes.c_int
+    lib.gpoeo_workspace_size_host.argtypes = [PP, ctypes.c_int64]
+    lib.gpoeo_workspace_size_host.restype = ctypes.c_size_t
+    lib.gpoeo_detect_periods_host.argtypes = [P, ctypes.c_int64, PP, P, ctypes.c_int64, P, ctypes.c_size_t, P]
+    lib.gpoeo_detect_periods_host.restype = ctypes.c_int
+    lib.gpoeo_power_spectrum.argtypes = [P, ctypes.c_int64, PP, P, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_power_spectrum.restype = ctypes.c_int
+    lib.gpoeo_similarity_workspace_size.argtypes = [ctypes.c_int64]
+    lib.gpoeo_similarity_workspace_size.restype = ctypes.c_size_t
+    lib.gpoeo_similarity_error.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, ctypes.c_int64, ctypes.c_int32,
+                                           ctypes.c_int32, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_similarity_error.restype = ctypes.c_int
+    lib.gpoeo_read_counters.argtypes = [P, PP, ctypes.c_int64, ctypes.POINTER(GpoeoCounters), P]
+    lib.gpoeo_read_counters.restype = ctypes.c_int
+    lib.gpoeo_status_string.argtypes = [ctypes.c_int]
+    lib.gpoeo_status_string.restype = ctypes.c_char_p
+    lib.gpoeo_version.argtypes = []
+    lib.gpoeo_version.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise GpoeoError(f"{what}: {load().gpoeo_status_string(rc).decode()} ({rc})")
+
+
+def default_params(n_samples: int, n_features: int = 1, sample_interval: float = 1.0, **kw) -> GpoeoParams:
+    """gpoeo_default_params, then override any field by keyword (weights=... for w_c)."""
+    p = GpoeoParams()
+    load().gpoeo_default_params(ctypes.byref(p), n_samples, n_features, sample_interval)
+    weights = kw.pop("weights", None)
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise KeyError(k)
+        setattr(p, k, v)
+    if weights is not None:
+        for i, w in enumerate(weights):
+            p.feature_weights[i] = w
+    return p
+
+
+def params_for(spec, **kw) -> GpoeoParams:
+    """Params for a workload-spec object (n_samples, n_features, min/max_period)."""
+    return default_params(spec.n_samples, spec.n_features, kw.pop("sample_interval", 1.0),
+                          min_period=spec.min_period, max_period=spec.max_period, **kw)
+
+
+def validate(p: GpoeoParams) -> int:
+    return load().gpoeo_validate_params(ctypes.byref(p))
+
+
+def workspace_size(p: GpoeoParams, batch: int) -> int:
+    return int(load().gpoeo_workspace_size(ctypes.byref(p), batch))
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def alloc_workspace(nbytes: int, device=None):
+    import torch
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device or "cuda")
+
+
+def detect_periods(traces, p: GpoeoParams, workspace=None, results=None, detail=False, stream=None):
+    """Alg. 1 on a CUDA float32 tensor of traces [B][trace_stride] (or [B][F][N]).
+
+    Returns (results uint8 tensor viewed as RESULT_DTYPE records, detail tensor or None,
+    workspace). Asynchronous on `stream` (default: torch's current stream).
+    """
+    import torch
+    assert traces.is_cuda and traces.dtype == torch.float32 and traces.is_contiguous()
+    B = traces.shape[0]
+    lib = load()
+    need = workspace_size(p, B)
+    if need == 0:
+        _check(validate(p), "params")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, traces.device)
+    if results is None:
+        results = torch.empty(B * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=traces.device)
+    det = torch.empty(B * DETAIL_DTYPE.itemsize, dtype=torch.uint8, device=traces.device) if detail else None
+    rc = lib.gpoeo_detect_periods_ex(ctypes.c_void_p(traces.data_ptr()), B, ctypes.byref(p),
+                                     ctypes.c_void_p(results.data_ptr()),
+                                     ctypes.c_void_p(det.data_ptr()) if det is not None else None,
+                                     ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_handle(stream))
+    _check(rc, "gpoeo_detect_periods")
+    return results, det, workspace
+
+
+def results_numpy(results) -> np.ndarray:
+    return results.cpu().numpy().view(RESULT_DTYPE)
+
+
+def detail_numpy(det) -> np.ndarray:
+    return det.cpu().numpy().view(DETAIL_DTYPE)
+
+
+def detect_periods_host(host_traces: np.ndarray, p: GpoeoParams, chunk: int = 4096, workspace=None, stream=None,
+                        out: np.ndarray | None = None) -> np.ndarray:
+    """End-to-end over HOST memory (pinned numpy/torch buffer recommended): chunked H2D
+    copies overlapped with compute inside the library; returns RESULT_DTYPE records."""
+    lib = load()
+    B = host_traces.shape[0]
+    chunk = max(1, min(chunk, B))
+    need = int(lib.gpoeo_workspace_size_host(ctypes.byref(p), chunk))
+    if need == 0:
+        _check(validate(p), "params")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need)
+    if out is None:
+        out = np.empty(B, dtype=RESULT_DTYPE)
+    ptr = host_traces.data_ptr() if hasattr(host_traces, "data_ptr") else host_traces.ctypes.data
+    rc = lib.gpoeo_detect_periods_host(ctypes.c_void_p(ptr), B, ctypes.byref(p), ctypes.c_void_p(out.ctypes.data),
+                                       chunk, ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                       _stream_handle(stream))
+    _check(rc, "gpoeo_detect_periods_host")
+    return out
+
+
+def power_spectrum(traces, p: GpoeoParams, want_signal=True, stream=None):
+    """(spectra [B][N/2+1] fp32, signal [B][N] fp32) on the device."""
+    import torch
+    B = traces.shape[0]
+    N = p.n_samples
+    lib = load()
+    ws = alloc_workspace(workspace_size(p, B) or 256, traces.device)
+    spectra = torch.empty((B, N // 2 + 1), dtype=torch.float32, device=traces.device)
+    signal = torch.empty((B, N), dtype=torch.float32, device=traces.device) if want_signal else None
+    rc = lib.gpoeo_power_spectrum(ctypes.c_void_p(traces.data_ptr()), B, ctypes.byref(p),
+                                  ctypes.c_void_p(spectra.data_ptr()),
+                                  ctypes.c_void_p(signal.data_ptr()) if signal is not None else None,
+                                  ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_handle(stream))
+    _check(rc, "gpoeo_power_spectrum")
+    return spectra, signal
+
+
+def similarity_error(signal, trace_index, period, num_groups: int = 4, gmm_max_iters: int = 32, stream=None):
+    """Alg. 2 Err(L) for queries (trace_index[q], period[q]) on signal [B][N] (CUDA fp32)."""
+    import torch
+    lib = load()
+    B, N = signal.shape
+    ti = torch.as_tensor(trace_index, dtype=torch.int32, device=signal.device).contiguous()
+    pe = torch.as_tensor(period, dtype=torch.int32, device=signal.device).contiguous()
+    nq = ti.numel()
+    out = torch.empty(nq, dtype=torch.float64, device=signal.device)
+    ws = alloc_workspace(int(lib.gpoeo_similarity_workspace_size(nq)), signal.device)
+    rc = lib.gpoeo_similarity_error(ctypes.c_void_p(signal.data_ptr()), B, N, ctypes.c_void_p(ti.data_ptr()),
+                                    ctypes.c_void_p(pe.data_ptr()), nq, num_groups, gmm_max_iters,
+                                    ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                    _stream_handle(stream))
+    _check(rc, "gpoeo_similarity_error")
+    return out
+
+
+def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:
+    c = GpoeoCounters()
+    _check(load().gpoeo_read_counters(ctypes.c_void_p(workspace.data_ptr()), ctypes.byref(p), batch,
+                                      ctypes.byref(c), _stream_handle(stream)), "gpoeo_read_counters")
+    return dict(n_candidate_queries=c.n_candidate_queries, n_local_queries=c.n_local_queries,
+                cem_sample_passes=c.cem_sample_passes)
+
+
+def version() -> int:
+    return load().gpoeo_version()

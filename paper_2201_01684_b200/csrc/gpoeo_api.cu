@@ -1,0 +1,409 @@
+// gpoeo_api.cu — the C ABI of include/gpoeo.h: validation, workspace layout, launch
+// sequence. Every compute step runs in the kernels of composite.cu / spectrum.cu /
+// score.cu / select.cu; this file only marshals.
+//
+// Launch sequence of gpoeo_detect_periods (one stream, no host sync, no allocation):
+//   memset(counters) -> composite (a1) -> spectrum+peaks (a2, a3; appends candidate
+//   queries) -> score(candidate queries) (a4) -> select (a5, a6; appends local queries)
+//   -> score(local queries) (a4) -> final (a7).
+#include <stdio.h>
+#include <string.h>
+
+#include "gpoeo_internal.cuh"
+
+using namespace gpoeo;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+
+int ilog2(int64_t v) {
+  int l = 0;
+  while ((1ll << l) < v) ++l;
+  return l;
+}
+
+void local_range(int64_t N, int64_t kb, int64_t Lmin, int64_t Lmax, int64_t* lo, int64_t* hi) {
+  const int64_t num = N * (N - 1);
+  int64_t l = num / ((N - 1) * kb + N);
+  int64_t h = num / ((N - 1) * kb - N);
+  if (l < Lmin) l = Lmin;
+  if (h > Lmax) h = Lmax;
+  *lo = l;
+  *hi = h;
+}
+
+int validate(const gpoeo_params* p) {
+  if (!p) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (!is_pow2(p->n_samples) || p->n_samples < (1 << GPOEO_MIN_LOG2N) || p->n_samples > (1 << GPOEO_MAX_LOG2N))
+    return GPOEO_ERR_UNSUPPORTED;
+  if (p->n_features < 1 || p->n_features > GPOEO_MAX_FEATURES) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->trace_stride < (int64_t)p->n_features * p->n_samples) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->trace_stride % 4 != 0) return GPOEO_ERR_MISALIGNED;
+  if (!(p->sample_interval > 0.0)) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->min_period < 2 || p->max_period < p->min_period || p->max_period > p->n_samples / 2)
+    return GPOEO_ERR_INVALID_ARGUMENT;
+  if (!(p->c_peak > 0.f) || p->c_peak > 1.f) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->max_candidates < 1 || p->max_candidates > GPOEO_MAX_CANDIDATES) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->num_groups < 1 || p->num_groups > GPOEO_MAX_GROUPS) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->gmm_max_iters < 1 || p->gmm_max_iters > 1000000) return GPOEO_ERR_INVALID_ARGUMENT;
+  return GPOEO_OK;
+}
+
+Plan make_plan(const gpoeo_params* p, int64_t batch) {
+  Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  pl.N = p->n_samples;
+  pl.F = p->n_features;
+  pl.log2N = ilog2(pl.N);
+  pl.n = pl.N / 2;
+  pl.C = pl.n > 16384 ? pl.n / 16384 : 1;
+  pl.n2 = pl.n / pl.C;
+  pl.log2n2 = ilog2(pl.n2);
+  pl.stride = p->trace_stride;
+  pl.Lmin = p->min_period;
+  pl.Lmax = p->max_period;
+  pl.K = p->max_candidates;
+  pl.G = p->num_groups;
+  pl.maxit = p->gmm_max_iters;
+  pl.c_peak = p->c_peak;
+  for (int c = 0; c < GPOEO_MAX_FEATURES; ++c) pl.w[c] = p->feature_weights[c];
+  pl.Ts = p->sample_interval;
+  pl.batch = batch;
+  // band (Z21): floor(N/k) <= Lmax  <=>  k >= floor(N/(Lmax+1)) + 1;  floor(N/k) >= Lmin <=> k <= floor(N/Lmin)
+  int64_t klo = (int64_t)pl.N / ((int64_t)pl.Lmax + 1) + 1;
+  int64_t khi = (int64_t)pl.N / pl.Lmin;
+  if (klo < 1) klo = 1;
+  if (khi > pl.n) khi = pl.n;
+  pl.k_lo = (int32_t)klo;
+  pl.k_hi = (int32_t)khi;
+  int64_t ml = 0;
+  for (int64_t k = klo; k <= khi; ++k) {
+    int64_t lo, hi;
+    local_range(pl.N, k, pl.Lmin, pl.Lmax, &lo, &hi);
+    if (hi - lo + 1 > ml) ml = hi - lo + 1;
+  }
+  pl.max_local = ml;
+  return pl;
+}
+
+struct Layout {
+  size_t off_y, off_status, off_ncand, off_ck, off_cL, off_cP, off_cerr, off_bb, off_llo, off_lhi, off_lbase,
+      off_ia, off_ib, off_lerr, off_lab, off_ctr, total;
+  int32_t lab_stride;
+};
+
+Layout layout(const Plan& pl) {
+  Layout L;
+  const size_t B = (size_t)pl.batch, K = (size_t)pl.K, ML = (size_t)pl.max_local;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  L.off_ctr = take(sizeof(unsigned long long) * kCounterSlots);
+  L.off_y = take(sizeof(float) * B * (size_t)pl.N);
+  L.off_status = take(sizeof(int32_t) * B);
+  L.off_ncand = take(sizeof(int32_t) * B);
+  L.off_ck = take(sizeof(int32_t) * B * K);
+  L.off_cL = take(sizeof(int32_t) * B * K);
+  L.off_cP = take(sizeof(float) * B * K);
+  L.off_cerr = take(sizeof(double) * B * K);
+  L.off_bb = take(sizeof(int32_t) * B);
+  L.off_llo = take(sizeof(int32_t) * B);
+  L.off_lhi = take(sizeof(int32_t) * B);
+  L.off_lbase = take(sizeof(int64_t) * B);
+  L.off_ia = take(sizeof(int4) * B * K);
+  L.off_ib = take(sizeof(int4) * B * ML);
+  L.off_lerr = take(sizeof(double) * B * ML);
+  L.lab_stride = pl.Lmax > kLabCap ? ((pl.Lmax + 15) & ~15) : 0;
+  L.off_lab = take((size_t)kMaxScoreCtas * (kScoreThreads / 32) * (size_t)L.lab_stride);
+  L.total = o;
+  return L;
+}
+
+Work carve(const Plan& pl, const Layout& L, void* ws) {
+  char* b = static_cast<char*>(ws);
+  Work w;
+  w.ctr = reinterpret_cast<unsigned long long*>(b + L.off_ctr);
+  w.y = reinterpret_cast<float*>(b + L.off_y);
+  w.status = reinterpret_cast<int32_t*>(b + L.off_status);
+  w.n_cand = reinterpret_cast<int32_t*>(b + L.off_ncand);
+  w.cand_k = reinterpret_cast<int32_t*>(b + L.off_ck);
+  w.cand_L = reinterpret_cast<int32_t*>(b + L.off_cL);
+  w.cand_P = reinterpret_cast<float*>(b + L.off_cP);
+  w.cand_err = reinterpret_cast<double*>(b + L.off_cerr);
+  w.best_bin = reinterpret_cast<int32_t*>(b + L.off_bb);
+  w.local_lo = reinterpret_cast<int32_t*>(b + L.off_llo);
+  w.local_hi = reinterpret_cast<int32_t*>(b + L.off_lhi);
+  w.local_base = reinterpret_cast<int64_t*>(b + L.off_lbase);
+  w.items_a = reinterpret_cast<int4*>(b + L.off_ia);
+  w.items_b = reinterpret_cast<int4*>(b + L.off_ib);
+  w.local_err = reinterpret_cast<double*>(b + L.off_lerr);
+  w.lab_scratch = L.lab_stride ? reinterpret_cast<uint8_t*>(b + L.off_lab) : nullptr;
+  (void)pl;
+  return w;
+}
+
+int check_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return GPOEO_ERR_CUDA;
+  }
+  return GPOEO_OK;
+}
+
+#define CK(expr)                          \
+  do {                                    \
+    cudaError_t e_ = (expr);              \
+    if (e_ != cudaSuccess) return GPOEO_ERR_CUDA; \
+  } while (0)
+
+int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, gpoeo_result* results,
+               gpoeo_detail* detail, cudaStream_t s) {
+  Work w = carve(pl, L, ws);
+  CK(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
+  if (pl.batch == 0) return GPOEO_OK;
+  CK(launch_composite(traces, pl, w.y, w.status, s));
+  CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
+  CK(launch_score(pl, w.y, w.items_a, &w.ctr[CTR_ITEMS_A], &w.ctr[CTR_CURSOR_A], w.cand_err, w.lab_scratch,
+                  L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
+  CK(launch_select(pl, w, s));
+  CK(launch_score(pl, w.y, w.items_b, &w.ctr[CTR_ITEMS_B], &w.ctr[CTR_CURSOR_B], w.local_err, w.lab_scratch,
+                  L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
+  CK(launch_final(pl, w, results, detail, s));
+  return GPOEO_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// pack (trace_index, period) into scorer items; count = n
+__global__ void pack_items_kernel(const int32_t* __restrict__ ti, const int32_t* __restrict__ per, int64_t n,
+                                  int4* __restrict__ items, unsigned long long* ctr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) ctr[CTR_ITEMS_A] = (unsigned long long)n;
+  if (i < n) items[i] = make_int4(ti[i], per[i], (int)i, 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+void gpoeo_default_params(gpoeo_params* p, int32_t n_samples, int32_t n_features, double sample_interval) {
+  if (!p) return;
+  memset(p, 0, sizeof(*p));
+  p->n_samples = n_samples;
+  p->n_features = n_features;
+  p->trace_stride = (((int64_t)n_features * n_samples) + 3) & ~(int64_t)3;
+  p->sample_interval = sample_interval;
+  p->min_period = 2;
+  p->max_period = n_samples / 2;
+  p->c_peak = 0.65f;
+  p->max_candidates = 16;
+  p->num_groups = 4;
+  p->gmm_max_iters = 32;
+  for (int c = 0; c < GPOEO_MAX_FEATURES; ++c) p->feature_weights[c] = 1.0f;
+}
+
+int gpoeo_validate_params(const gpoeo_params* p) { return validate(p); }
+
+size_t gpoeo_workspace_size(const gpoeo_params* p, int64_t batch) {
+  if (validate(p) != GPOEO_OK || batch < 0) return 0;
+  return layout(make_plan(p, batch)).total;
+}
+
+int gpoeo_detect_periods_ex(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
+                            gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!traces || !results)) return GPOEO_ERR_INVALID_ARGUMENT;
+  const Plan pl = make_plan(p, batch);
+  const Layout L = layout(pl);
+  if (!workspace || workspace_bytes < L.total) return GPOEO_ERR_WORKSPACE;
+  if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if ((double)batch * (double)(pl.max_local > pl.K ? pl.max_local : pl.K) >= 2147483647.0)
+    return GPOEO_ERR_INVALID_ARGUMENT;  // item slots are int32: split the batch
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  return run_detect(traces, pl, L, workspace, results, detail, static_cast<cudaStream_t>(stream));
+}
+
+int gpoeo_detect_periods(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  return gpoeo_detect_periods_ex(traces, batch, p, results, nullptr, workspace, workspace_bytes, stream);
+}
+
+size_t gpoeo_workspace_size_host(const gpoeo_params* p, int64_t chunk) {
+  if (validate(p) != GPOEO_OK || chunk < 1) return 0;
+  const Plan pl = make_plan(p, chunk);
+  const size_t inner = layout(pl).total;
+  const size_t tr = align_up(sizeof(float) * (size_t)p->trace_stride * (size_t)chunk);
+  const size_t rs = align_up(sizeof(gpoeo_result) * (size_t)chunk);
+  return 2 * tr + 2 * rs + 2 * inner;
+}
+
+int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpoeo_params* p,
+                              gpoeo_result* host_results, int64_t chunk, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0 || chunk < 1) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!host_traces || !host_results)) return GPOEO_ERR_INVALID_ARGUMENT;
+  const size_t need = gpoeo_workspace_size_host(p, chunk);
+  if (!workspace || workspace_bytes < need) return GPOEO_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Plan full = make_plan(p, chunk);
+  const size_t inner = layout(full).total;
+  const size_t tr = align_up(sizeof(float) * (size_t)p->trace_stride * (size_t)chunk);
+  const size_t rs = align_up(sizeof(gpoeo_result) * (size_t)chunk);
+  char* base = static_cast<char*>(workspace);
+  float* dtr[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + tr)};
+  gpoeo_result* dres[2] = {reinterpret_cast<gpoeo_result*>(base + 2 * tr),
+                           reinterpret_cast<gpoeo_result*>(base + 2 * tr + rs)};
+  void* dws[2] = {base + 2 * tr + 2 * rs, base + 2 * tr + 2 * rs + inner};
+  cudaStream_t cs;
+  cudaEvent_t copied[2], done[2];
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return GPOEO_ERR_CUDA;
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+  }
+  int rc = GPOEO_OK;
+  // the copy stream must not start before work already queued on `s` that the caller
+  // expects to precede this call
+  cudaEvent_t start;
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventRecord(start, s);
+  cudaStreamWaitEvent(cs, start, 0);
+  int64_t nchunks = (batch + chunk - 1) / chunk;
+  for (int64_t c = 0; c < nchunks && rc == GPOEO_OK; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t first = c * chunk;
+    const int64_t n = batch - first < chunk ? batch - first : chunk;
+    if (c >= 2) cudaStreamWaitEvent(cs, done[b], 0);  // buffer b free again
+    if (cudaMemcpyAsync(dtr[b], host_traces + first * p->trace_stride, sizeof(float) * (size_t)p->trace_stride * n,
+                        cudaMemcpyHostToDevice, cs) != cudaSuccess)
+      rc = GPOEO_ERR_CUDA;
+    cudaEventRecord(copied[b], cs);
+    cudaStreamWaitEvent(s, copied[b], 0);
+    const Plan pl = make_plan(p, n);
+    const Layout L = layout(pl);
+    if (rc == GPOEO_OK) rc = run_detect(dtr[b], pl, L, dws[b], dres[b], nullptr, s);
+    if (rc == GPOEO_OK &&
+        cudaMemcpyAsync(host_results + first, dres[b], sizeof(gpoeo_result) * n, cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess)
+      rc = GPOEO_ERR_CUDA;
+    cudaEventRecord(done[b], s);
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess) rc = GPOEO_ERR_CUDA;
+  cudaStreamSynchronize(cs);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(done[i]);
+  }
+  cudaEventDestroy(start);
+  cudaStreamDestroy(cs);
+  return rc;
+}
+
+int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params* p, float* spectra, float* signal,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && !traces) return GPOEO_ERR_INVALID_ARGUMENT;
+  const Plan pl = make_plan(p, batch);
+  const Layout L = layout(pl);
+  if (!workspace || workspace_bytes < L.total) return GPOEO_ERR_WORKSPACE;
+  if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace) || (signal && !aligned16(signal)))
+    return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Work w = carve(pl, L, workspace);
+  if (batch == 0) return GPOEO_OK;
+  float* y = signal ? signal : w.y;
+  CK(launch_composite(traces, pl, y, w.status, s));
+  if (spectra) CK(launch_spectrum(pl, y, w.status, w, spectra, false, s));
+  return GPOEO_OK;
+}
+
+size_t gpoeo_similarity_workspace_size(int64_t n_queries) {
+  if (n_queries < 0) return 0;
+  size_t o = align_up(sizeof(unsigned long long) * kCounterSlots);
+  o += align_up(sizeof(int4) * (size_t)(n_queries > 0 ? n_queries : 1));
+  // label scratch sized for the largest supported L (only used when L > kLabCap)
+  o += align_up((size_t)kMaxScoreCtas * (kScoreThreads / 32) * (size_t)((1 << GPOEO_MAX_LOG2N) / 2));
+  return o;
+}
+
+int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples, const int32_t* trace_index,
+                           const int32_t* period, int64_t n_queries, int32_t num_groups, int32_t gmm_max_iters,
+                           double* error_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!is_pow2(n_samples) || n_samples < (1 << GPOEO_MIN_LOG2N) || n_samples > (1 << GPOEO_MAX_LOG2N))
+    return GPOEO_ERR_UNSUPPORTED;
+  if (batch < 0 || n_queries < 0 || num_groups < 1 || num_groups > GPOEO_MAX_GROUPS || gmm_max_iters < 1)
+    return GPOEO_ERR_INVALID_ARGUMENT;
+  if (n_queries > 0 && (!signal || !trace_index || !period || !error_out)) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (n_queries >= 2147483647) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < gpoeo_similarity_workspace_size(n_queries)) return GPOEO_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  if (n_queries == 0) return GPOEO_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* b = static_cast<char*>(workspace);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(b);
+  int4* items = reinterpret_cast<int4*>(b + align_up(sizeof(unsigned long long) * kCounterSlots));
+  uint8_t* lab = reinterpret_cast<uint8_t*>(b + align_up(sizeof(unsigned long long) * kCounterSlots) +
+                                            align_up(sizeof(int4) * (size_t)n_queries));
+  Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  pl.N = n_samples;
+  pl.G = num_groups;
+  pl.maxit = gmm_max_iters;
+  pl.batch = batch;
+  CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
+  pack_items_kernel<<<(unsigned)((n_queries + 255) / 256), 256, 0, s>>>(trace_index, period, n_queries, items, ctr);
+  CK(cudaGetLastError());
+  const int32_t maxL = n_samples / 2;
+  CK(launch_score(pl, signal, items, &ctr[CTR_ITEMS_A], &ctr[CTR_CURSOR_A], error_out, lab,
+                  ((maxL + 15) & ~15), &ctr[CTR_CEM_PASSES], maxL, s));
+  return GPOEO_OK;
+}
+
+int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t batch, gpoeo_counters* out,
+                        void* stream) {
+  if (!workspace || !out) return GPOEO_ERR_INVALID_ARGUMENT;
+  (void)p;
+  (void)batch;
+  unsigned long long h[kCounterSlots];
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(h, workspace, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess) return GPOEO_ERR_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return GPOEO_ERR_CUDA;
+  out->n_candidate_queries = (int64_t)h[CTR_ITEMS_A];
+  out->n_local_queries = (int64_t)h[CTR_ITEMS_B];
+  out->cem_sample_passes = (int64_t)h[CTR_CEM_PASSES];
+  return GPOEO_OK;
+}
+
+const char* gpoeo_status_string(int status) {
+  switch (status) {
+    case GPOEO_OK: return "ok";
+    case GPOEO_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case GPOEO_ERR_UNSUPPORTED: return "unsupported (n_samples must be a power of two in [2^3, 2^18])";
+    case GPOEO_ERR_WORKSPACE: return "workspace missing or too small";
+    case GPOEO_ERR_MISALIGNED: return "misaligned pointer or stride";
+    case GPOEO_ERR_CUDA: return "CUDA error (no device or launch failure)";
+    default: return "unknown status";
+  }
+}
+
+int gpoeo_version(void) { return GPOEO_API_VERSION; }
+
+}  // extern "C"

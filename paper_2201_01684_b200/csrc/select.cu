@@ -1,0 +1,104 @@
+// select.cu — rows a5, a6, a7: arg-best candidate (Alg.1 l.9-10), the local
+// refinement range (Alg.1 l.11-13, readings Z17-Z19) and the final argmin
+// + per-trace result (Alg.1 l.18-19, Z20).
+//
+// Local range around the fractional centre Tc = N/k_b (T_s = 1; T_s never changes the
+// integer result, Z25):  N_T = (N-1)/Tc,
+//   T_low = Tc (1 - 1/(N_T+1)) = N(N-1) / ((N-1) k_b + N),
+//   T_up  = Tc (1 + 1/(N_T-1)) = N(N-1) / ((N-1) k_b - N),
+// evaluated at the integers floor(T_low) .. floor(T_up) (T_accu = T_s), clipped to
+// [L_min, L_max]; exact int64 division.
+#include "gpoeo_internal.cuh"
+
+namespace gpoeo {
+
+// One thread per trace: argmin (Err, L) over candidates, local range, work-list append.
+__global__ void select_kernel(Plan p, Work w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= p.batch) return;
+  if (w.status[t] != GPOEO_TRACE_OK) return;
+  const int nc = w.n_cand[t];
+  int best = 0;
+  for (int c = 1; c < nc; ++c) {
+    const double e = w.cand_err[t * p.K + c], eb = w.cand_err[t * p.K + best];
+    if (e < eb || (e == eb && w.cand_L[t * p.K + c] < w.cand_L[t * p.K + best])) best = c;
+  }
+  const int64_t kb = w.cand_k[t * p.K + best];
+  const int64_t N = p.N;
+  const int64_t num = N * (N - 1);
+  int64_t lo = num / ((N - 1) * kb + N);
+  int64_t hi = num / ((N - 1) * kb - N);
+  if (lo < p.Lmin) lo = p.Lmin;
+  if (hi > p.Lmax) hi = p.Lmax;
+  const int64_t cnt = hi - lo + 1;
+  const unsigned long long base = atomicAdd(&w.ctr[CTR_ITEMS_B], (unsigned long long)cnt);
+  w.best_bin[t] = (int32_t)kb;
+  w.local_lo[t] = (int32_t)lo;
+  w.local_hi[t] = (int32_t)hi;
+  w.local_base[t] = (int64_t)base;
+  for (int64_t i = 0; i < cnt; ++i)
+    w.items_b[base + i] = make_int4((int)t, (int)(lo + i), (int)(base + i), 0);
+}
+
+// One thread per trace: argmin (Err, L) over the local range -> result (+ detail).
+__global__ void final_kernel(Plan p, Work w, gpoeo_result* __restrict__ res, gpoeo_detail* __restrict__ det) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= p.batch) return;
+  const int32_t st = w.status[t];
+  gpoeo_result r;
+  r.status = st;
+  r.period = -1;
+  r.period_s = 0.f;
+  r.error = 0.f;
+  r.best_candidate = -1;
+  r.n_candidates = (st == GPOEO_TRACE_OK || st == GPOEO_TRACE_APERIODIC) ? w.n_cand[t] : 0;
+  double eb = 0.0;
+  int32_t lo = 0, hi = -1, kb = -1;
+  if (st == GPOEO_TRACE_OK) {
+    lo = w.local_lo[t];
+    hi = w.local_hi[t];
+    kb = w.best_bin[t];
+    const double* le = w.local_err + w.local_base[t];
+    int32_t Lb = lo;
+    eb = le[0];
+    for (int32_t L = lo + 1; L <= hi; ++L) {
+      const double e = le[L - lo];
+      if (e < eb) { eb = e; Lb = L; }  // strict: ties keep the smaller L (Z17)
+    }
+    r.period = Lb;
+    r.period_s = (float)((double)Lb * p.Ts);
+    r.error = (float)eb;
+    r.best_candidate = p.N / kb;
+  }
+  res[t] = r;
+  if (det) {
+    gpoeo_detail d;
+    d.n_candidates = r.n_candidates;
+    d.best_bin = kb;
+    d.local_lo = lo;
+    d.local_hi = hi;
+    for (int c = 0; c < GPOEO_MAX_CANDIDATES; ++c) {
+      const bool v = c < r.n_candidates && c < p.K;
+      d.cand_k[c] = v ? w.cand_k[t * p.K + c] : 0;
+      d.cand_L[c] = v ? w.cand_L[t * p.K + c] : 0;
+      d.cand_P[c] = v ? w.cand_P[t * p.K + c] : 0.f;
+      d.cand_err[c] = (v && st == GPOEO_TRACE_OK) ? w.cand_err[t * p.K + c] : 0.0;
+    }
+    d.best_err = eb;
+    det[t] = d;
+  }
+}
+
+cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s) {
+  if (p.batch == 0) return cudaSuccess;
+  select_kernel<<<(unsigned)((p.batch + 127) / 128), 128, 0, s>>>(p, w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final(const Plan& p, Work w, gpoeo_result* results, gpoeo_detail* detail, cudaStream_t s) {
+  if (p.batch == 0) return cudaSuccess;
+  final_kernel<<<(unsigned)((p.batch + 127) / 128), 128, 0, s>>>(p, w, results, detail);
+  return cudaGetLastError();
+}
+
+}  // namespace gpoeo

@@ -106,3 +106,15 @@ def test_composite_identical_sinusoids():
     assert int(np.argmax(P)) == 1024 // 64
     y1, _, _, _ = O.composite(s[None])
     np.testing.assert_allclose(y, 3 * y1, rtol=1e-6, atol=1e-6)
+
+
+def test_band_only_dft_same_values():
+    # the band-only evaluation computes the same per-bin arithmetic, only fewer bins
+    rng = np.random.default_rng(1)
+    y = rng.standard_normal(2048).astype(np.float32)
+    P = O.power_spectrum(y)
+    np.testing.assert_array_equal(O.power_spectrum_bins(y, 100, 300), P[100:301])
+    x = (rng.standard_normal((1, 2048)) * 5 + np.sin(np.arange(2048) * 2 * np.pi / 41)).astype(np.float32)
+    a = O.detect(x, O.Params(2048, 1, min_period=10, max_period=400))
+    b = O.detect(x, O.Params(2048, 1, min_period=10, max_period=400, dft_band_only=True))
+    assert a.period == b.period and a.cand_L == b.cand_L and a.error == b.error and a.margins == b.margins
