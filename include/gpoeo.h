@@ -125,6 +125,16 @@ int gpoeo_detect_periods(const float* traces, int64_t batch, const gpoeo_params*
 int gpoeo_detect_periods_ex(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
                             gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Same as gpoeo_detect_periods_ex, and records 7 caller-created cudaEvent_t (passed as
+ * void*, may be NULL) on `stream` at the phase boundaries, for live per-kernel timing:
+ *   [0] start  [1] after composite (a1)  [2] after spectrum+peaks (a2,a3)
+ *   [3] after candidate scoring (a4)  [4] after select (a5,a6)  [5] after local scoring (a4)
+ *   [6] after final (a7).  Still sync-free and allocation-free. */
+#define GPOEO_NUM_PHASE_EVENTS 7
+int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
+                               gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream,
+                               void* const* phase_events);
+
 /* End-to-end variant over HOST buffers (the e2e path of bench.py):
  *  host_traces  HOST [batch][trace_stride] fp32 (pinned memory gives async overlap);
  *  host_results HOST [batch] gpoeo_result.

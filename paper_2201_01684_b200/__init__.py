@@ -85,6 +85,8 @@ def load():
     lib.gpoeo_detect_periods.restype = ctypes.c_int
     lib.gpoeo_detect_periods_ex.argtypes = [P, ctypes.c_int64, PP, P, P, P, ctypes.c_size_t, P]
     lib.gpoeo_detect_periods_ex.restype = ctypes.c_int
+    lib.gpoeo_detect_periods_timed.argtypes = [P, ctypes.c_int64, PP, P, P, P, ctypes.c_size_t, P, P]
+    lib.gpoeo_detect_periods_timed.restype = ctypes.c_int
     lib.gpoeo_workspace_size_host.argtypes = [PP, ctypes.c_int64]
     lib.gpoeo_workspace_size_host.restype = ctypes.c_size_t
     lib.gpoeo_detect_periods_host.argtypes = [P, ctypes.c_int64, PP, P, ctypes.c_int64, P, ctypes.c_size_t, P]
@@ -178,6 +180,20 @@ def detect_periods(traces, p: GpoeoParams, workspace=None, results=None, detail=
                                      ctypes.c_void_p(workspace.data_ptr()), workspace.numel(), _stream_handle(stream))
     _check(rc, "gpoeo_detect_periods")
     return results, det, workspace
+
+
+PHASES = ("composite", "spectrum_peaks", "score_candidates", "select", "score_local", "final")
+
+
+def detect_periods_timed(traces, p: GpoeoParams, workspace, results, events, stream=None):
+    """gpoeo_detect_periods_timed with 7 torch.cuda.Event(enable_timing=True) objects
+    (already recorded once so their handles exist); returns nothing (async)."""
+    arr = (ctypes.c_void_p * 7)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    rc = load().gpoeo_detect_periods_timed(ctypes.c_void_p(traces.data_ptr()), traces.shape[0], ctypes.byref(p),
+                                           ctypes.c_void_p(results.data_ptr()), None,
+                                           ctypes.c_void_p(workspace.data_ptr()), workspace.numel(),
+                                           _stream_handle(stream), arr)
+    _check(rc, "gpoeo_detect_periods_timed")
 
 
 def results_numpy(results) -> np.ndarray:

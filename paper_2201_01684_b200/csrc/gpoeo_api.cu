@@ -165,18 +165,29 @@ int check_device() {
   } while (0)
 
 int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, gpoeo_result* results,
-               gpoeo_detail* detail, cudaStream_t s) {
+               gpoeo_detail* detail, cudaStream_t s, void* const* ev = nullptr) {
+  auto mark = [&](int i) -> cudaError_t {
+    return (ev && ev[i]) ? cudaEventRecord(static_cast<cudaEvent_t>(ev[i]), s) : cudaSuccess;
+  };
   Work w = carve(pl, L, ws);
+  CK(mark(0));
   CK(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
-  if (pl.batch == 0) return GPOEO_OK;
-  CK(launch_composite(traces, pl, w.y, w.status, s));
-  CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
-  CK(launch_score(pl, w.y, w.items_a, &w.ctr[CTR_ITEMS_A], &w.ctr[CTR_CURSOR_A], w.cand_err, w.lab_scratch,
-                  L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
-  CK(launch_select(pl, w, s));
-  CK(launch_score(pl, w.y, w.items_b, &w.ctr[CTR_ITEMS_B], &w.ctr[CTR_CURSOR_B], w.local_err, w.lab_scratch,
-                  L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
-  CK(launch_final(pl, w, results, detail, s));
+  if (pl.batch > 0) CK(launch_composite(traces, pl, w.y, w.status, s));
+  CK(mark(1));
+  if (pl.batch > 0) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
+  CK(mark(2));
+  if (pl.batch > 0)
+    CK(launch_score(pl, w.y, w.items_a, &w.ctr[CTR_ITEMS_A], &w.ctr[CTR_CURSOR_A], w.cand_err, w.lab_scratch,
+                    L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
+  CK(mark(3));
+  if (pl.batch > 0) CK(launch_select(pl, w, s));
+  CK(mark(4));
+  if (pl.batch > 0)
+    CK(launch_score(pl, w.y, w.items_b, &w.ctr[CTR_ITEMS_B], &w.ctr[CTR_CURSOR_B], w.local_err, w.lab_scratch,
+                    L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
+  CK(mark(5));
+  if (pl.batch > 0) CK(launch_final(pl, w, results, detail, s));
+  CK(mark(6));
   return GPOEO_OK;
 }
 
@@ -219,6 +230,12 @@ size_t gpoeo_workspace_size(const gpoeo_params* p, int64_t batch) {
 
 int gpoeo_detect_periods_ex(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
                             gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream) {
+  return gpoeo_detect_periods_timed(traces, batch, p, results, detail, workspace, workspace_bytes, stream, nullptr);
+}
+
+int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,
+                               gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream,
+                               void* const* phase_events) {
   int v = validate(p);
   if (v != GPOEO_OK) return v;
   if (batch < 0) return GPOEO_ERR_INVALID_ARGUMENT;
@@ -230,7 +247,7 @@ int gpoeo_detect_periods_ex(const float* traces, int64_t batch, const gpoeo_para
   if ((double)batch * (double)(pl.max_local > pl.K ? pl.max_local : pl.K) >= 2147483647.0)
     return GPOEO_ERR_INVALID_ARGUMENT;  // item slots are int32: split the batch
   if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
-  return run_detect(traces, pl, L, workspace, results, detail, static_cast<cudaStream_t>(stream));
+  return run_detect(traces, pl, L, workspace, results, detail, static_cast<cudaStream_t>(stream), phase_events);
 }
 
 int gpoeo_detect_periods(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,

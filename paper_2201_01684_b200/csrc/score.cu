@@ -11,40 +11,45 @@
 // equal), ties -> lowest j; stop when no label changes or after gmm_max_iters passes;
 // M-step: dead if empty, pi = n/L, mu = mean, var = max(mean sq. dev., 1e-6 R^2).
 //
-// GPU organisation (persistent CTAs of 256 threads; one query at a time per CTA):
-//  * L <= 512: the pair is owned by a "team" of tau = pow2ceil(ceil(L/16)) <= 32 lanes;
-//    each lane holds <= 16 samples of W_i in fp64 registers across all CEM passes.
-//  * L  > 512: a warp owns a pair; samples are streamed from L1/L2 each pass and labels
-//    live in shared memory (global scratch beyond 8192 samples).
-//  * Team reductions are xor-butterflies (every lane ends with the identical sum), all
-//    loops are warp-uniform so converged teams idle through their neighbours' passes.
-//  * Sufficient statistics are fp64: n_j, S_j = sum y, Q_j = sum (y - mu_j)^2 (shifted
-//    by the pass's own mu_j so the variance does not cancel). W_{i+1} is reduced with
-//    the same lane order as W_i, so identical windows give RelPrev == RelBack exactly
-//    (Z28) and exactly periodic input scores exactly 0.
+// GPU organisation (persistent CTAs of 256 threads, one query at a time per CTA):
+//  * A pair (W_i, W_{i+1}) is owned by a team of tau = pow2ceil(ceil(L/16)) lanes
+//    (1 .. 256: sub-warp, warp, or 2/4/8-warp teams); each lane keeps its <= 16 samples
+//    of W_i in fp64 registers for all CEM passes: the trace is read from L2 once per pair.
+//  * Per pass, a lane accumulates fp64 sufficient statistics of its samples: n_j,
+//    S_j = sum y, Q_j = sum (y - mu_j)^2 (shifted by the pass's own mu_j: no cancellation).
+//    Teams reduce them with xor butterflies (every lane ends with the identical sum);
+//    multi-warp teams add the per-warp sums through shared memory in warp order behind a
+//    named barrier. The M-step of component j runs on one lane and is broadcast.
+//  * All loops are warp-uniform; converged sub-warp teams idle through their neighbours'
+//    passes. W_{i+1} is reduced with the same lane order as W_i, so identical windows give
+//    RelPrev == RelBack exactly (Z28) and exactly periodic input scores exactly 0.
+//  * L > 16*256: a warp owns the pair and streams samples from L1/L2 every pass (labels in
+//    shared memory or global scratch).
 //  * Err(L) is the sum of per-team partial sums in team order: deterministic.
 #include "gpoeo_internal.cuh"
 
 namespace gpoeo {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kWarps = kScoreThreads / 32;
+constexpr int kRegMaxL = kLpt * kScoreThreads;  // 4096: register path limit
 
 template <typename V>
-__device__ __forceinline__ V team_sum(V v, int tau) {
-  for (int off = tau >> 1; off; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
+__device__ __forceinline__ V xor_sum(V v, int width) {
+  for (int off = width >> 1; off; off >>= 1) v += __shfl_xor_sync(FULL, v, off);
   return v;
 }
-__device__ __forceinline__ double team_min(double v, int tau) {
-  for (int off = tau >> 1; off; off >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, off));
+__device__ __forceinline__ double xor_min(double v, int width) {
+  for (int off = width >> 1; off; off >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, off));
   return v;
 }
-__device__ __forceinline__ double team_max(double v, int tau) {
-  for (int off = tau >> 1; off; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
+__device__ __forceinline__ double xor_max(double v, int width) {
+  for (int off = width >> 1; off; off >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, off));
   return v;
 }
-__device__ __forceinline__ int team_or(int v, int tau) {
-  for (int off = tau >> 1; off; off >>= 1) v |= __shfl_xor_sync(FULL, v, off);
-  return v;
+
+__device__ __forceinline__ void named_barrier(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ double smape(double a, double b) {
@@ -52,16 +57,43 @@ __device__ __forceinline__ double smape(double a, double b) {
   return den == 0.0 ? 0.0 : fabs(a - b) / den;
 }
 
-// CEM model of one window (identical in every lane of the team).
+// Team all-reduce of NV doubles (identical result in every lane of the team).
+// tau <= 32: xor butterfly. tau >= 64: warp butterfly, then per-warp sums through smem
+// (red[buf][warp][v]) added in warp order by lane v, then broadcast from lane v.
+template <int NV>
+__device__ __forceinline__ void team_allreduce(double* v, int tau, int team, int lane, int warp, double* red,
+                                               int& buf) {
+  if (tau <= 32) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = xor_sum(v[i], tau);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = xor_sum(v[i], 32);
+  const int W = tau >> 5;
+  const int w0 = (warp / W) * W;
+  double* slot = red + buf * (kWarps * 32);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) slot[warp * 32 + i] = v[i];
+  }
+  named_barrier(1 + team, tau);
+  double s = 0.0;
+  if (lane < NV)
+    for (int w = 0; w < W; ++w) s += slot[(w0 + w) * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = __shfl_sync(FULL, s, i);
+  buf ^= 1;
+}
+
+// CEM model of one window (identical in every lane of the team). Dead components carry
+// c = -inf, h = 0 so the assignment needs no liveness test.
 template <int G>
 struct Cem {
   double mu[G], c[G], h[G];
-  unsigned alive;
   double floor_var;
-  int32_t L;
 
-  __device__ __forceinline__ void init(double mn, double R, int32_t L_) {
-    L = L_;
+  __device__ __forceinline__ void init(double mn, double R) {
     const double w = R / (double)G;
 #pragma unroll
     for (int j = 0; j < G; ++j) {
@@ -69,168 +101,198 @@ struct Cem {
       c[j] = 0.0;
       h[j] = 0.0;
     }
-    alive = (1u << G) - 1u;
     floor_var = __dmul_rn(__dmul_rn(1e-6, R), R);
   }
 
-  // label of y for pass `it` (1-based); e = (y - mu_label)^2
-  __device__ __forceinline__ int assign(double y, int it, double& e_out) const {
+  // label of y for pass `it` (1-based); e[j] = (y - mu_j)^2
+  __device__ __forceinline__ int assign(double y, int it, double* e) const {
     int best = 0;
-    double bs = 0.0, be = 0.0;
-    bool first = true;
+    double bs;
     if (it == 1) {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
         const double d = __dsub_rn(y, mu[j]);
-        const double e = __dmul_rn(d, d);
-        if (first || e < bs) { best = j; bs = e; be = e; }
-        first = false;
+        e[j] = __dmul_rn(d, d);
       }
+      bs = e[0];
+#pragma unroll
+      for (int j = 1; j < G; ++j)
+        if (e[j] < bs) { best = j; bs = e[j]; }
     } else {
+      double sc[G];
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        if (!((alive >> j) & 1u)) continue;
         const double d = y - mu[j];
-        const double e = d * d;
-        const double sc = fma(-e, h[j], c[j]);
-        if (first || sc > bs) { best = j; bs = sc; be = e; }
-        first = false;
+        e[j] = d * d;
+        sc[j] = fma(-e[j], h[j], c[j]);
       }
-    }
-    e_out = be;
-    return best;
-  }
-
-  // M-step from team-reduced stats of the pass that used the current mu.
-  __device__ __forceinline__ void update(const int32_t* n, const double* S, const double* Q) {
+      bs = sc[0];
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      if (!((alive >> j) & 1u)) continue;
-      if (n[j] == 0) {
-        alive &= ~(1u << j);
-        continue;
-      }
-      const double nj = (double)n[j];
-      const double m = S[j] / nj;
-      const double dm = m - mu[j];
-      double var = Q[j] / nj - dm * dm;
-      if (var < floor_var) var = floor_var;
-      mu[j] = m;
-      c[j] = log(nj / (double)L) - 0.5 * log(var);
-      h[j] = 0.5 / var;
+      for (int j = 1; j < G; ++j)
+        if (sc[j] > bs) { best = j; bs = sc[j]; }
     }
+    return best;
   }
 };
 
-// ---------------------------------------------------------------------------------
-// Register mode: team of tau lanes, <= kLpt samples per lane. All lanes of the warp run
-// the same number of loop trips; `has` masks teams without a pair.
+// M-step from the reduced v = [n_0..n_{G-1}, S_0.., Q_0.., changed]: component j is
+// updated on lane (j mod lanes) of the team and broadcast (one log per component per pass).
 template <int G>
-__device__ double pair_err_reg(const float* __restrict__ A, int32_t L, int tau, int lane_t, bool has, int maxit,
-                               long long& passes_out) {
+__device__ __forceinline__ void mstep(Cem<G>& cem, const double* v, int L, int tau, int lane) {
+  const int lanes = tau < 32 ? tau : 32;
+  const int lt = lane & (lanes - 1);
+  const int base = lane & ~(lanes - 1);
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    double mu = cem.mu[j], c = cem.c[j], h = cem.h[j];
+    if ((j % lanes) == lt) {
+      const double nj = v[j];
+      if (nj == 0.0) {
+        c = -INFINITY;  // dead (stays dead)
+        h = 0.0;
+      } else {
+        const double m = v[G + j] / nj;
+        const double dm = m - mu;
+        double var = v[2 * G + j] / nj - dm * dm;
+        if (var < cem.floor_var) var = cem.floor_var;
+        mu = m;
+        c = log(nj / (double)L) - 0.5 * log(var);
+        h = 0.5 / var;
+      }
+    }
+    const int src = base + (j % lanes);
+    cem.mu[j] = __shfl_sync(FULL, mu, src);
+    cem.c[j] = __shfl_sync(FULL, c, src);
+    cem.h[j] = __shfl_sync(FULL, h, src);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// One pair in register mode. `has` is team-uniform; loops are warp-uniform.
+template <int G>
+__device__ double pair_err_reg(const float* __restrict__ A, int32_t L, int tau, int lt, int team, int lane, int warp,
+                               bool has, int maxit, double* red, int& buf, long long& passes_out) {
+  constexpr int NV = 3 * G + 1;
   double yv[kLpt];
   uint64_t labs = 0;  // kLpt 4-bit labels
-  const int cnt = has ? (L - lane_t + tau - 1) / tau : 0;
+  const int cnt = has ? (L - lt + tau - 1) / tau : 0;
   double mn = INFINITY, mx = -INFINITY, TA = 0.0;
 #pragma unroll
   for (int u = 0; u < kLpt; ++u) {
     yv[u] = 0.0;
     if (u < cnt) {
-      yv[u] = (double)__ldg(A + lane_t + u * tau);
+      yv[u] = (double)__ldg(A + lt + u * tau);
       mn = fmin(mn, yv[u]);
       mx = fmax(mx, yv[u]);
       TA += yv[u];
     }
   }
-  mn = team_min(mn, tau);
-  mx = team_max(mx, tau);
-  TA = team_sum(TA, tau);
+  {
+    // (min, -max, sum) over the team
+    const int w = tau < 32 ? tau : 32;
+    double a = xor_min(mn, w), b = xor_min(-mx, w), s = xor_sum(TA, w);
+    if (tau > 32) {
+      const int W = tau >> 5, w0 = (warp / W) * W;
+      double* slot = red + buf * (kWarps * 32);
+      if (lane == 0) {
+        slot[warp * 32 + 0] = a;
+        slot[warp * 32 + 1] = b;
+        slot[warp * 32 + 2] = s;
+      }
+      named_barrier(1 + team, tau);
+      a = INFINITY;
+      b = INFINITY;
+      s = 0.0;
+      for (int k = 0; k < W; ++k) {
+        a = fmin(a, slot[(w0 + k) * 32 + 0]);
+        b = fmin(b, slot[(w0 + k) * 32 + 1]);
+        s += slot[(w0 + k) * 32 + 2];
+      }
+      buf ^= 1;
+    }
+    mn = a;
+    mx = -b;
+    TA = s;
+  }
   const double R = mx - mn;
   const bool clustered = has && (R > 0.0) && (G > 1);
   bool active = clustered;
   Cem<G> cem;
-  cem.init(mn, R, L);
+  cem.init(mn, R);
   int passes = 0;
   for (int it = 1; it <= maxit; ++it) {
     if (!__any_sync(FULL, active)) break;
-    int32_t n[G];
-    double S[G], Q[G];
-    int changed = 0;
+    double v[NV];
 #pragma unroll
-    for (int j = 0; j < G; ++j) { n[j] = 0; S[j] = 0.0; Q[j] = 0.0; }
+    for (int i = 0; i < NV; ++i) v[i] = 0.0;
     if (active) {
+      int32_t n[G];
+      int changed = 0;
+#pragma unroll
+      for (int j = 0; j < G; ++j) n[j] = 0;
 #pragma unroll
       for (int u = 0; u < kLpt; ++u) {
         if (u < cnt) {
-          double e;
+          double e[G];
           const int b = cem.assign(yv[u], it, e);
           const int old = (int)((labs >> (4 * u)) & 15u);
           changed |= (b != old);
           labs = (labs & ~(15ull << (4 * u))) | ((uint64_t)b << (4 * u));
 #pragma unroll
           for (int j = 0; j < G; ++j)
-            if (b == j) { n[j] += 1; S[j] += yv[u]; Q[j] += e; }
+            if (b == j) { n[j] += 1; v[G + j] += yv[u]; v[2 * G + j] += e[j]; }
         }
       }
-    }
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      n[j] = team_sum(n[j], tau);
-      S[j] = team_sum(S[j], tau);
-      Q[j] = team_sum(Q[j], tau);
+      for (int j = 0; j < G; ++j) v[j] = (double)n[j];
+      v[3 * G] = (double)changed;
     }
-    changed = team_or(changed, tau);
+    team_allreduce<NV>(v, tau, team, lane, warp, red, buf);
     if (active) {
       passes = it;
-      if ((it > 1 && !changed) || it == maxit) {
-        active = false;  // converged (or capped): labels are final
-      } else {
-        cem.update(n, S, Q);
-      }
+      if ((it > 1 && v[3 * G] == 0.0) || it == maxit) active = false;  // labels final
     }
+    if (__any_sync(FULL, active)) mstep<G>(cem, v, L, tau, lane);  // finished teams ignore it
   }
-  // Final groups on W_i and the same index sets on W_{i+1}, in one pass with the same
-  // lane order for both windows (Z28: identical windows -> identical sums).
-  int32_t nA[G];
-  double SA[G], SB[G], TB = 0.0;
+  // Final groups on W_i and the same index sets on W_{i+1}, one pass, same lane order for
+  // both windows (Z28: identical windows -> identical sums).
+  double v[NV];  // nA[G], SA[G], SB[G], TB
 #pragma unroll
-  for (int j = 0; j < G; ++j) { nA[j] = 0; SA[j] = 0.0; SB[j] = 0.0; }
+  for (int i = 0; i < NV; ++i) v[i] = 0.0;
   if (clustered) {
     const float* B = A + L;
+    int32_t n[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) n[j] = 0;
 #pragma unroll
     for (int u = 0; u < kLpt; ++u) {
       if (u < cnt) {
-        const double yb = (double)__ldg(B + lane_t + u * tau);
-        TB += yb;
+        const double yb = (double)__ldg(B + lt + u * tau);
+        v[3 * G] += yb;
         const int l = (int)((labs >> (4 * u)) & 15u);
 #pragma unroll
         for (int j = 0; j < G; ++j)
-          if (l == j) { nA[j] += 1; SA[j] += yv[u]; SB[j] += yb; }
+          if (l == j) { n[j] += 1; v[G + j] += yv[u]; v[2 * G + j] += yb; }
       }
     }
-  }
 #pragma unroll
-  for (int j = 0; j < G; ++j) {
-    nA[j] = team_sum(nA[j], tau);
-    SA[j] = team_sum(SA[j], tau);
-    SB[j] = team_sum(SB[j], tau);
+    for (int j = 0; j < G; ++j) v[j] = (double)n[j];
   }
-  TB = team_sum(TB, tau);
+  team_allreduce<NV>(v, tau, team, lane, warp, red, buf);
   if (!clustered) return 0.0;
-  if (lane_t == 0) passes_out += (long long)(passes + 1) * L;
-  const double mA = TA / (double)L, mB = TB / (double)L;
+  if (lt == 0) passes_out += (long long)(passes + 1) * L;
+  const double mA = TA / (double)L, mB = v[3 * G] / (double)L;
   double num = 0.0;
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    if (nA[j] == 0) continue;
-    const double nj = (double)nA[j];
-    num += nj * smape(SA[j] / nj - mA, SB[j] / nj - mB);
+    if (v[j] == 0.0) continue;
+    num += v[j] * smape(v[G + j] / v[j] - mA, v[2 * G + j] / v[j] - mB);
   }
   return num / (double)L;
 }
 
 // ---------------------------------------------------------------------------------
-// Warp mode (L > kSubwarpMaxL): one warp per pair; samples streamed from L1/L2.
+// Streaming warp mode (L > kRegMaxL): one warp per pair; samples re-read from L1/L2.
 template <int G>
 __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane, uint8_t* lab, int maxit,
                                 long long& passes_out) {
@@ -241,13 +303,13 @@ __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane
     mx = fmax(mx, v);
     TA += v;
   }
-  mn = team_min(mn, 32);
-  mx = team_max(mx, 32);
-  TA = team_sum(TA, 32);
+  mn = xor_min(mn, 32);
+  mx = xor_max(mx, 32);
+  TA = xor_sum(TA, 32);
   const double R = mx - mn;
   if (!(R > 0.0) || G == 1) return 0.0;
   Cem<G> cem;
-  cem.init(mn, R, L);
+  cem.init(mn, R);
   int passes = 0;
   for (int it = 1; it <= maxit; ++it) {
     int32_t n[G];
@@ -257,54 +319,48 @@ __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane
     for (int j = 0; j < G; ++j) { n[j] = 0; S[j] = 0.0; Q[j] = 0.0; }
     for (int s = lane; s < L; s += 32) {
       const double v = (double)__ldg(A + s);
-      double e;
+      double e[G];
       const int b = cem.assign(v, it, e);
       if (it > 1) changed |= (b != lab[s]);
       lab[s] = (uint8_t)b;
 #pragma unroll
       for (int j = 0; j < G; ++j)
-        if (b == j) { n[j] += 1; S[j] += v; Q[j] += e; }
+        if (b == j) { n[j] += 1; S[j] += v; Q[j] += e[j]; }
     }
+    double v[3 * G + 1];
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      n[j] = team_sum(n[j], 32);
-      S[j] = team_sum(S[j], 32);
-      Q[j] = team_sum(Q[j], 32);
+      v[j] = xor_sum((double)n[j], 32);
+      v[G + j] = xor_sum(S[j], 32);
+      v[2 * G + j] = xor_sum(Q[j], 32);
     }
-    changed = team_or(changed, 32);
+    changed = xor_sum(changed, 32);
     passes = it;
     if ((it > 1 && !changed) || it == maxit) break;
-    cem.update(n, S, Q);
+    mstep<G>(cem, v, L, 32, lane);
   }
-  int32_t nA[G];
-  double SA[G], SB[G], TB = 0.0;
+  double v[3 * G + 1];
 #pragma unroll
-  for (int j = 0; j < G; ++j) { nA[j] = 0; SA[j] = 0.0; SB[j] = 0.0; }
+  for (int i = 0; i < 3 * G + 1; ++i) v[i] = 0.0;
   const float* B = A + L;
   for (int s = lane; s < L; s += 32) {
     const double ya = (double)__ldg(A + s);
     const double yb = (double)__ldg(B + s);
-    TB += yb;
+    v[3 * G] += yb;
     const int l = lab[s];
 #pragma unroll
     for (int j = 0; j < G; ++j)
-      if (l == j) { nA[j] += 1; SA[j] += ya; SB[j] += yb; }
+      if (l == j) { v[j] += 1.0; v[G + j] += ya; v[2 * G + j] += yb; }
   }
 #pragma unroll
-  for (int j = 0; j < G; ++j) {
-    nA[j] = team_sum(nA[j], 32);
-    SA[j] = team_sum(SA[j], 32);
-    SB[j] = team_sum(SB[j], 32);
-  }
-  TB = team_sum(TB, 32);
+  for (int i = 0; i < 3 * G + 1; ++i) v[i] = xor_sum(v[i], 32);
   if (lane == 0) passes_out += (long long)(passes + 1) * L;
-  const double mA = TA / (double)L, mB = TB / (double)L;
+  const double mA = TA / (double)L, mB = v[3 * G] / (double)L;
   double num = 0.0;
 #pragma unroll
   for (int j = 0; j < G; ++j) {
-    if (nA[j] == 0) continue;
-    const double nj = (double)nA[j];
-    num += nj * smape(SA[j] / nj - mA, SB[j] / nj - mB);
+    if (v[j] == 0.0) continue;
+    num += v[j] * smape(v[G + j] / v[j] - mA, v[2 * G + j] / v[j] - mB);
   }
   return num / (double)L;
 }
@@ -317,9 +373,9 @@ struct ScoreArgs {
   const unsigned long long* count;
   unsigned long long* cursor;
   double* err_out;
-  uint8_t* lab_scratch;  // [gridDim][8 warps][lab_stride] when L > kLabCap
+  uint8_t* lab_scratch;  // [gridDim][8 warps][lab_stride] when L > lab_cap
   int32_t lab_stride;
-  int32_t lab_cap;       // bytes of smem labels per warp
+  int32_t lab_cap;       // bytes of smem labels per warp (streaming mode)
   unsigned long long* cem_ctr;
 };
 
@@ -327,49 +383,49 @@ template <int G>
 __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(ScoreArgs a) {
   __shared__ int64_t s_item;
   __shared__ double s_team[kScoreThreads];
-  extern __shared__ uint8_t s_lab[];  // [8 warps][lab_cap] (warp mode, L <= lab_cap)
+  __shared__ double s_red[2 * kWarps * 32];
+  extern __shared__ uint8_t s_lab[];  // [8 warps][lab_cap] (streaming mode, L <= lab_cap)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long total = *a.count;
   long long passes = 0;
+  int buf = 0;
   for (;;) {
     if (tid == 0) s_item = (int64_t)atomicAdd(a.cursor, 1ull);
     __syncthreads();
     const int64_t item = s_item;
     __syncthreads();
     if ((unsigned long long)item >= total) break;
+    buf = 0;  // teams are re-formed per query: every warp restarts the reduction parity
     const int4 q = a.items[item];
     const int64_t t = q.x;
     const int32_t L = q.y;
-    const int32_t M = a.N / L;
-    const int32_t npairs = M - 1;
+    const int32_t npairs = a.N / L - 1;
     const float* yt = a.y + t * (int64_t)a.N;
     double acc = 0.0;
-    int nteams, team;
-    if (L <= kSubwarpMaxL) {
-      int tau = 1;
+    int tau;
+    if (L <= kRegMaxL) {
+      tau = 1;
       while (tau * kLpt < L) tau <<= 1;
-      nteams = kScoreThreads / tau;
-      team = tid / tau;
-      const int lane_t = tid & (tau - 1);
-      // warp-uniform trip count: the warp's teams are team0 .. team0 + 32/tau - 1
-      const int team0 = (warp * 32) / tau;
+      const int nteams = kScoreThreads / tau;
+      const int team = tid / tau;
+      const int lt = tid & (tau - 1);
+      // warp-uniform trip count (sub-warp teams of one warp: team0 .. team0 + 32/tau - 1)
+      const int team0 = tau >= 32 ? team : (warp * 32) / tau;
       const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
       for (int i = 0; i < trips; ++i) {
         const int pidx = team + i * nteams;
         const bool has = pidx < npairs;
         const float* A = yt + (int64_t)(has ? pidx : 0) * L;
-        const double e = pair_err_reg<G>(A, L, tau, lane_t, has, a.maxit, passes);
+        const double e = pair_err_reg<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, passes);
         if (has) acc += e;
       }
-      if (lane_t != 0) acc = 0.0;
+      if (lt != 0) acc = 0.0;
     } else {
-      nteams = kScoreThreads / 32;
-      team = warp;
+      tau = 32;
       uint8_t* lab = (L <= a.lab_cap) ? s_lab + (int64_t)warp * a.lab_cap
-                                    : a.lab_scratch + ((int64_t)blockIdx.x * (kScoreThreads / 32) + warp) * a.lab_stride;
-      for (int pidx = warp; pidx < npairs; pidx += nteams) {
-        const double e = pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
-        acc += e;
+                                      : a.lab_scratch + ((int64_t)blockIdx.x * kWarps + warp) * a.lab_stride;
+      for (int pidx = warp; pidx < npairs; pidx += kWarps) {
+        acc += pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
         __syncwarp();
       }
       if (lane != 0) acc = 0.0;
@@ -378,39 +434,43 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(ScoreArgs a) {
     s_team[tid] = acc;
     __syncthreads();
     if (tid == 0) {
-      const int tau = kScoreThreads / nteams;
       double sum = 0.0;
-      for (int tm = 0; tm < nteams; ++tm) sum += s_team[tm * tau];
+      for (int tm = 0; tm < kScoreThreads; tm += tau) sum += s_team[tm];
       a.err_out[q.z] = sum / (double)npairs;
     }
     __syncthreads();
   }
-  // work counter: one atomic per thread that did work
   for (int off = 16; off; off >>= 1) passes += __shfl_xor_sync(FULL, passes, off);
   if (lane == 0 && passes) atomicAdd(a.cem_ctr, (unsigned long long)passes);
 }
 
 template <int G>
-static int grid_for() {
+static int grid_for(size_t smem) {
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_kernel<G>, kScoreThreads,
-                                                (size_t)kLabCap * (kScoreThreads / 32));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_kernel<G>, kScoreThreads, smem);
   if (occ < 1) occ = 1;
   return sms * occ < kMaxScoreCtas ? sms * occ : kMaxScoreCtas;
 }
 
+static size_t score_smem(int32_t max_L, int32_t* lab_cap) {
+  int32_t cap = 0;
+  if (max_L > kRegMaxL) cap = ((max_L < kLabCap ? max_L : kLabCap) + 15) & ~15;
+  if (lab_cap) *lab_cap = cap;
+  return (size_t)cap * kWarps;
+}
+
 int score_grid(int G) {
   switch (G) {
-    case 1: return grid_for<1>();
-    case 2: return grid_for<2>();
-    case 3: return grid_for<3>();
-    case 4: return grid_for<4>();
-    case 5: return grid_for<5>();
-    case 6: return grid_for<6>();
-    case 7: return grid_for<7>();
-    default: return grid_for<8>();
+    case 1: return grid_for<1>(0);
+    case 2: return grid_for<2>(0);
+    case 3: return grid_for<3>(0);
+    case 4: return grid_for<4>(0);
+    case 5: return grid_for<5>(0);
+    case 6: return grid_for<6>(0);
+    case 7: return grid_for<7>(0);
+    default: return grid_for<8>(0);
   }
 }
 
@@ -418,17 +478,15 @@ cudaError_t launch_score(const Plan& p, const float* y, const int4* items, const
                          unsigned long long* cursor, double* err_out, uint8_t* lab_scratch, int32_t lab_stride,
                          unsigned long long* cem_ctr, int32_t max_L, cudaStream_t s) {
   int32_t lab_cap = 0;
-  if (max_L > kSubwarpMaxL) lab_cap = ((max_L < kLabCap ? max_L : kLabCap) + 15) & ~15;
-  const size_t smem = (size_t)lab_cap * (kScoreThreads / 32);
+  const size_t smem = score_smem(max_L, &lab_cap);
   ScoreArgs a{y, p.N, p.maxit, items, count, cursor, err_out, lab_scratch, lab_stride, lab_cap, cem_ctr};
-  const int grid = score_grid(p.G);
-#define GPOEO_SCORE_CASE(GG)                                                                         \
-  case GG: {                                                                                       \
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                         (int)smem);                                               \
-    if (e != cudaSuccess) return e;                                                                \
-    score_kernel<GG><<<grid, kScoreThreads, smem, s>>>(a);                                         \
-    break;                                                                                         \
+#define GPOEO_SCORE_CASE(GG)                                                                              \
+  case GG: {                                                                                            \
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                         (int)smem);                                                    \
+    if (e != cudaSuccess) return e;                                                                     \
+    score_kernel<GG><<<grid_for<GG>(smem), kScoreThreads, smem, s>>>(a);                                \
+    break;                                                                                              \
   }
   switch (p.G) {
     GPOEO_SCORE_CASE(1)

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
     if (threadIdx.x == 0) {
       w.n_cand[t] = nc;
       int32_t status = st;
+      if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;  // empty band (Z21)
       if (status == GPOEO_TRACE_OK && nc == 0) status = GPOEO_TRACE_APERIODIC;
       w.status[t] = status;
       if (status == GPOEO_TRACE_OK) {
