@@ -30,6 +30,10 @@
 
 namespace gpoeo {
 
+#ifndef GPOEO_SCORE_MINB
+#define GPOEO_SCORE_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kWarps = kScoreThreads / 32;
 constexpr int kRegMaxL = kLpt * kScoreThreads;  // 4096: register path limit
@@ -60,16 +64,22 @@ __device__ __forceinline__ double smape(double a, double b) {
 // Team all-reduce of NV doubles (identical result in every lane of the team).
 // tau <= 32: xor butterfly. tau >= 64: warp butterfly, then per-warp sums through smem
 // (red[buf][warp][v]) added in warp order by lane v, then broadcast from lane v.
+// xor-butterfly all-reduce of NV doubles over aligned groups of `width` lanes; the level
+// loop is rolled (one copy of the NV shuffles per call site keeps the code small).
+template <int NV>
+__device__ __forceinline__ void xor_sum_vec(double* v, int width) {
+#pragma unroll 1
+  for (int off = width >> 1; off; off >>= 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(FULL, v[i], off);
+  }
+}
+
 template <int NV>
 __device__ __forceinline__ void team_allreduce(double* v, int tau, int team, int lane, int warp, double* red,
                                                int& buf) {
-  if (tau <= 32) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = xor_sum(v[i], tau);
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = xor_sum(v[i], 32);
+  xor_sum_vec<NV>(v, tau < 32 ? tau : 32);
+  if (tau <= 32) return;
   const int W = tau >> 5;
   const int w0 = (warp / W) * W;
   double* slot = red + buf * (kWarps * 32);
@@ -104,93 +114,116 @@ struct Cem {
     floor_var = __dmul_rn(__dmul_rn(1e-6, R), R);
   }
 
-  // label of y for pass `it` (1-based); e[j] = (y - mu_j)^2
-  __device__ __forceinline__ int assign(double y, int it, double* e) const {
-    int best = 0;
-    double bs;
-    if (it == 1) {
+  // first pass: every pi_j, var_j equal -> argmin (y - mu_j)^2 on exactly rounded values
+  __device__ __forceinline__ int assign_first(double y, double* e) const {
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const double d = __dsub_rn(y, mu[j]);
-        e[j] = __dmul_rn(d, d);
-      }
-      bs = e[0];
-#pragma unroll
-      for (int j = 1; j < G; ++j)
-        if (e[j] < bs) { best = j; bs = e[j]; }
-    } else {
-      double sc[G];
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        const double d = y - mu[j];
-        e[j] = d * d;
-        sc[j] = fma(-e[j], h[j], c[j]);
-      }
-      bs = sc[0];
-#pragma unroll
-      for (int j = 1; j < G; ++j)
-        if (sc[j] > bs) { best = j; bs = sc[j]; }
+    for (int j = 0; j < G; ++j) {
+      const double d = __dsub_rn(y, mu[j]);
+      e[j] = __dmul_rn(d, d);
     }
+    int best = 0;
+    double bs = e[0];
+#pragma unroll
+    for (int j = 1; j < G; ++j)
+      if (e[j] < bs) { best = j; bs = e[j]; }
     return best;
+  }
+
+  // later passes: argmax ln pi_j - 1/2 ln var_j - (y - mu_j)^2/(2 var_j); e[j] = (y - mu_j)^2
+  __device__ __forceinline__ int assign(double y, double* e) const {
+    double sc[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const double d = y - mu[j];
+      e[j] = d * d;
+      sc[j] = fma(-e[j], h[j], c[j]);
+    }
+    int best = 0;
+    double bs = sc[0];
+#pragma unroll
+    for (int j = 1; j < G; ++j)
+      if (sc[j] > bs) { best = j; bs = sc[j]; }
+    return best;
+  }
+
+  __device__ __forceinline__ int assign(double y, int it, double* e) const {
+    return it == 1 ? assign_first(y, e) : assign(y, e);
   }
 };
 
-// M-step from the reduced v = [n_0..n_{G-1}, S_0.., Q_0.., changed]: component j is
-// updated on lane (j mod lanes) of the team and broadcast (one log per component per pass).
+// M-step from the reduced v = [n_0..n_{G-1}, S_0.., Q_0.., changed]. Component j is
+// updated on lane (j mod lanes) of the team (one log per component per pass) and
+// broadcast with shuffles, so every lane holds identical parameters.
 template <int G>
 __device__ __forceinline__ void mstep(Cem<G>& cem, const double* v, int L, int tau, int lane) {
   const int lanes = tau < 32 ? tau : 32;
   const int lt = lane & (lanes - 1);
-  const int base = lane & ~(lanes - 1);
+  const int base = lane - lt;
+  const int rounds = (G + lanes - 1) / lanes;
+#pragma unroll 1
+  for (int r = 0; r < rounds; ++r) {
+    const int j = lt + r * lanes;  // this lane's component in this round (>= G: none)
+    double nj = 0.0, S = 0.0, Q = 0.0, mu = 0.0, c = -INFINITY;
 #pragma unroll
-  for (int j = 0; j < G; ++j) {
-    double mu = cem.mu[j], c = cem.c[j], h = cem.h[j];
-    if ((j % lanes) == lt) {
-      const double nj = v[j];
+    for (int k = 0; k < G; ++k)
+      if (k == j) { nj = v[k]; S = v[G + k]; Q = v[2 * G + k]; mu = cem.mu[k]; c = cem.c[k]; }
+    double h = 0.0;
+    if (j < G) {
       if (nj == 0.0) {
         c = -INFINITY;  // dead (stays dead)
-        h = 0.0;
       } else {
-        const double m = v[G + j] / nj;
+        const double m = S / nj;
         const double dm = m - mu;
-        double var = v[2 * G + j] / nj - dm * dm;
+        double var = Q / nj - dm * dm;
         if (var < cem.floor_var) var = cem.floor_var;
+        const double p = nj / (double)L;
         mu = m;
-        c = log(nj / (double)L) - 0.5 * log(var);
+        c = 0.5 * log(p * p / var);  // ln pi - 1/2 ln var
         h = 0.5 / var;
       }
     }
-    const int src = base + (j % lanes);
-    cem.mu[j] = __shfl_sync(FULL, mu, src);
-    cem.c[j] = __shfl_sync(FULL, c, src);
-    cem.h[j] = __shfl_sync(FULL, h, src);
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      if (k / lanes == r) {
+        const int src = base + (k - r * lanes);
+        cem.mu[k] = __shfl_sync(FULL, mu, src);
+        cem.c[k] = __shfl_sync(FULL, c, src);
+        cem.h[k] = __shfl_sync(FULL, h, src);
+      }
+    }
   }
 }
 
 // ---------------------------------------------------------------------------------
-// One pair in register mode. `has` is team-uniform; loops are warp-uniform.
+// One pair, samples resident in shared memory. Lane lt of the team owns samples
+// s = lt + u*tau, u < cnt, stored at ys[u * kScoreThreads] (conflict-free: consecutive
+// threads, consecutive 8-byte words). Loops are rolled (small code: the whole scorer
+// fits the instruction cache); `has` is team-uniform; every loop with a shuffle or a
+// barrier is warp-uniform.
 template <int G>
-__device__ double pair_err_reg(const float* __restrict__ A, int32_t L, int tau, int lt, int team, int lane, int warp,
-                               bool has, int maxit, double* red, int& buf, long long& passes_out) {
+__device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau, int lt, int team, int lane, int warp,
+                                bool has, int maxit, double* red, int& buf, double* ys, long long& passes_out) {
   constexpr int NV = 3 * G + 1;
-  double yv[kLpt];
-  uint64_t labs = 0;  // kLpt 4-bit labels
   const int cnt = has ? (L - lt + tau - 1) / tau : 0;
   double mn = INFINITY, mx = -INFINITY, TA = 0.0;
-#pragma unroll
-  for (int u = 0; u < kLpt; ++u) {
-    yv[u] = 0.0;
-    if (u < cnt) {
-      yv[u] = (double)__ldg(A + lt + u * tau);
-      mn = fmin(mn, yv[u]);
-      mx = fmax(mx, yv[u]);
-      TA += yv[u];
-    }
+#pragma unroll 1
+  for (int u = 0; u < cnt; ++u) {
+    const double y = (double)__ldg(A + lt + u * tau);
+    ys[u * kScoreThreads] = y;
+    mn = fmin(mn, y);
+    mx = fmax(mx, y);
+    TA += y;
   }
   {
     // (min, -max, sum) over the team
     const int w = tau < 32 ? tau : 32;
-    double a = xor_min(mn, w), b = xor_min(-mx, w), s = xor_sum(TA, w);
+    double a = mn, b = -mx, s = TA;
+#pragma unroll 1
+    for (int off = w >> 1; off; off >>= 1) {
+      a = fmin(a, __shfl_xor_sync(FULL, a, off));
+      b = fmin(b, __shfl_xor_sync(FULL, b, off));
+      s += __shfl_xor_sync(FULL, s, off);
+    }
     if (tau > 32) {
       const int W = tau >> 5, w0 = (warp / W) * W;
       double* slot = red + buf * (kWarps * 32);
@@ -219,6 +252,7 @@ __device__ double pair_err_reg(const float* __restrict__ A, int32_t L, int tau, 
   bool active = clustered;
   Cem<G> cem;
   cem.init(mn, R);
+  uint64_t labs = 0;  // 4-bit labels of the lane's <= 16 samples
   int passes = 0;
   for (int it = 1; it <= maxit; ++it) {
     if (!__any_sync(FULL, active)) break;
@@ -230,17 +264,30 @@ __device__ double pair_err_reg(const float* __restrict__ A, int32_t L, int tau, 
       int changed = 0;
 #pragma unroll
       for (int j = 0; j < G; ++j) n[j] = 0;
-#pragma unroll
-      for (int u = 0; u < kLpt; ++u) {
-        if (u < cnt) {
+      if (it == 1) {
+#pragma unroll 1
+        for (int u = 0; u < cnt; ++u) {
+          const double y = ys[u * kScoreThreads];
           double e[G];
-          const int b = cem.assign(yv[u], it, e);
-          const int old = (int)((labs >> (4 * u)) & 15u);
-          changed |= (b != old);
-          labs = (labs & ~(15ull << (4 * u))) | ((uint64_t)b << (4 * u));
+          const int b = cem.assign_first(y, e);
+          labs |= (uint64_t)b << (4 * u);
 #pragma unroll
           for (int j = 0; j < G; ++j)
-            if (b == j) { n[j] += 1; v[G + j] += yv[u]; v[2 * G + j] += e[j]; }
+            if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
+        }
+      } else {
+#pragma unroll 1
+        for (int u = 0; u < cnt; ++u) {
+          const double y = ys[u * kScoreThreads];
+          double e[G];
+          const int b = cem.assign(y, e);
+          const int sh = 4 * u;
+          const int old = (int)((labs >> sh) & 15u);
+          changed |= (b != old);
+          labs ^= (uint64_t)(old ^ b) << sh;
+#pragma unroll
+          for (int j = 0; j < G; ++j)
+            if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
         }
       }
 #pragma unroll
@@ -264,16 +311,15 @@ __device__ double pair_err_reg(const float* __restrict__ A, int32_t L, int tau, 
     int32_t n[G];
 #pragma unroll
     for (int j = 0; j < G; ++j) n[j] = 0;
+#pragma unroll 1
+    for (int u = 0; u < cnt; ++u) {
+      const double ya = ys[u * kScoreThreads];
+      const double yb = (double)__ldg(B + lt + u * tau);
+      v[3 * G] += yb;
+      const int l = (int)((labs >> (4 * u)) & 15u);
 #pragma unroll
-    for (int u = 0; u < kLpt; ++u) {
-      if (u < cnt) {
-        const double yb = (double)__ldg(B + lt + u * tau);
-        v[3 * G] += yb;
-        const int l = (int)((labs >> (4 * u)) & 15u);
-#pragma unroll
-        for (int j = 0; j < G; ++j)
-          if (l == j) { n[j] += 1; v[G + j] += yv[u]; v[2 * G + j] += yb; }
-      }
+      for (int j = 0; j < G; ++j)
+        if (l == j) { n[j] += 1; v[G + j] += ya; v[2 * G + j] += yb; }
     }
 #pragma unroll
     for (int j = 0; j < G; ++j) v[j] = (double)n[j];
@@ -330,11 +376,13 @@ __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane
     double v[3 * G + 1];
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      v[j] = xor_sum((double)n[j], 32);
-      v[G + j] = xor_sum(S[j], 32);
-      v[2 * G + j] = xor_sum(Q[j], 32);
+      v[j] = (double)n[j];
+      v[G + j] = S[j];
+      v[2 * G + j] = Q[j];
     }
-    changed = xor_sum(changed, 32);
+    v[3 * G] = (double)changed;
+    xor_sum_vec<3 * G + 1>(v, 32);
+    changed = v[3 * G] != 0.0;
     passes = it;
     if ((it > 1 && !changed) || it == maxit) break;
     mstep<G>(cem, v, L, 32, lane);
@@ -352,8 +400,7 @@ __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane
     for (int j = 0; j < G; ++j)
       if (l == j) { v[j] += 1.0; v[G + j] += ya; v[2 * G + j] += yb; }
   }
-#pragma unroll
-  for (int i = 0; i < 3 * G + 1; ++i) v[i] = xor_sum(v[i], 32);
+  xor_sum_vec<3 * G + 1>(v, 32);
   if (lane == 0) passes_out += (long long)(passes + 1) * L;
   const double mA = TA / (double)L, mB = v[3 * G] / (double)L;
   double num = 0.0;
@@ -380,10 +427,11 @@ struct ScoreArgs {
 };
 
 template <int G>
-__global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(ScoreArgs a) {
   __shared__ int64_t s_item;
   __shared__ double s_team[kScoreThreads];
   __shared__ double s_red[2 * kWarps * 32];
+  __shared__ double s_ys[kLpt * kScoreThreads];  // register-path samples, [u][thread]
   extern __shared__ uint8_t s_lab[];  // [8 warps][lab_cap] (streaming mode, L <= lab_cap)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long total = *a.count;
@@ -416,7 +464,8 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(ScoreArgs a) {
         const int pidx = team + i * nteams;
         const bool has = pidx < npairs;
         const float* A = yt + (int64_t)(has ? pidx : 0) * L;
-        const double e = pair_err_reg<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, passes);
+        const double e =
+            pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
         if (has) acc += e;
       }
       if (lt != 0) acc = 0.0;

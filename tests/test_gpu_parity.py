@@ -44,8 +44,8 @@ def _compare(res, det, ods, label=""):
         amb = d.ambiguous()
         if amb:
             n_amb += 1
-        if d.status == O.TRACE_APERIODIC:
-            assert r["n_candidates"] == 0
+        if d.status != O.TRACE_OK:
+            assert r["n_candidates"] == 0 and r["period"] == -1
             continue
         if not amb or d.margins["d_thr"] >= 1e-5 and d.margins["d_peak"] >= 1e-5 and d.margins["d_rank"] >= 1e-5:
             nc = d.n_candidates
