@@ -120,7 +120,7 @@ Layout layout(const Plan& pl) {
   L.off_ia = take(sizeof(int4) * B * K);
   L.off_ib = take(sizeof(int4) * B * ML);
   L.off_lerr = take(sizeof(double) * B * ML);
-  L.lab_stride = pl.Lmax > kLabCap ? ((pl.Lmax + 15) & ~15) : 0;
+  L.lab_stride = pl.Lmax > kLabCap ? ((pl.Lmax + 15) & ~15) : 0;  // streaming path (L > 8192)
   L.off_lab = take((size_t)kMaxScoreCtas * (kScoreThreads / 32) * (size_t)L.lab_stride);
   L.total = o;
   return L;

@@ -36,7 +36,6 @@ namespace gpoeo {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kWarps = kScoreThreads / 32;
-constexpr int kRegMaxL = kLpt * kScoreThreads;  // 4096: register path limit
 
 template <typename V>
 __device__ __forceinline__ V xor_sum(V v, int width) {
@@ -338,6 +337,352 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 }
 
 // ---------------------------------------------------------------------------------
+// Bucketed warp mode (kBucketMinL <= L <= kBucketMaxL): one warp per pair.
+//
+// A CEM pass only needs, per component j, (n_j, sum y, sum (y - mu_j)^2) over the
+// samples it wins, and whether any label changed. The label of a sample depends only on
+// its value, and in exact arithmetic the winner changes only where two component scores
+// cross: at the real roots of s_j(y) - s_k(y), a quadratic per pair (<= G(G-1) roots).
+// The window's values are counting-sorted once into K value buckets (stable, warp
+// multisplit); each bucket keeps its member range, [min, max] and shifted sums
+// (sum (y - c_b), sum (y - c_b)^2, c_b = its first member). Per pass, a bucket whose
+// [min - delta, max + delta] holds no root is "whole": every member gets the label the
+// per-sample rule gives at the bucket minimum, and its statistics come from the bucket
+// sums (sum (y - mu)^2 = S2 + (c - mu)(2 S1 + n (c - mu)), no cancellation). Members of
+// the few buckets that straddle a root (delta = 1e-6 R absorbs root rounding) are
+// evaluated one by one with exactly the per-sample rule of the register path. Labels are
+// kept per sorted slot so "no label changed" is exact. The final W_i / W_{i+1} pass walks
+// the slots in one order for both windows (Z28). Decisions equal the per-sample
+// evaluation except at sub-rounding margins (Z27). Cost per pass: O(K + straddled
+// samples) instead of O(L).
+constexpr int kBuckets = 128;
+constexpr int kBucketMinL = kLpt * 16 + 1;  // 257: above this the pair is bucketed
+constexpr int kBucketMaxL = 8192;
+
+__host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
+  return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) +
+         (size_t)(kBuckets + 1) * 2 + 14 + (size_t)kBuckets * 2 + (size_t)kBuckets * 4 * 3 + (size_t)kBuckets * 8 * 2 +
+         kBuckets + 64;
+}
+
+struct BucketView {
+  uint16_t* pos;   // [Lcap] sorted slot -> sample index in the window
+  uint8_t* lab;    // [Lcap] label of each sorted slot
+  uint16_t* off;   // [K+1] first slot of bucket b
+  uint16_t* cur;   // [K]   scatter cursors
+  float* bmin;     // [K]
+  float* bmax;     // [K]
+  float* cb;       // [K]   shift (first member's value)
+  double* s1;      // [K]   sum (y - c_b)
+  double* s2;      // [K]   sum (y - c_b)^2
+  uint8_t* blab;   // [K]   whole-bucket label, 0xFF per-sample, 0xFE unset
+
+  __device__ static BucketView carve(uint8_t* base, int Lcap) {
+    BucketView v;
+    uint8_t* p = base;
+    v.pos = reinterpret_cast<uint16_t*>(p);
+    p += ((size_t)Lcap * 2 + 15) & ~(size_t)15;
+    v.lab = p;
+    p += ((size_t)Lcap + 15) & ~(size_t)15;
+    v.s1 = reinterpret_cast<double*>(p);
+    p += (size_t)kBuckets * 8;
+    v.s2 = reinterpret_cast<double*>(p);
+    p += (size_t)kBuckets * 8;
+    v.bmin = reinterpret_cast<float*>(p);
+    p += (size_t)kBuckets * 4;
+    v.bmax = reinterpret_cast<float*>(p);
+    p += (size_t)kBuckets * 4;
+    v.cb = reinterpret_cast<float*>(p);
+    p += (size_t)kBuckets * 4;
+    v.off = reinterpret_cast<uint16_t*>(p);
+    p += (size_t)(kBuckets + 1) * 2 + 14;
+    v.cur = reinterpret_cast<uint16_t*>(p);
+    p += (size_t)kBuckets * 2;
+    v.blab = p;
+    return v;
+  }
+};
+
+// Real roots of s_j(y) = s_k(y) with s(y) = c - h (y - mu)^2, in coordinates z = y - m0.
+__device__ __forceinline__ void score_crossings(double muj, double cj, double hj, double muk, double ck, double hk,
+                                                double m0, double& r0, double& r1) {
+  r0 = r1 = NAN;
+  if (cj == -INFINITY || ck == -INFINITY) return;  // a dead component never wins
+  const double uj = muj - m0, uk = muk - m0;
+  const double A = hk - hj;
+  const double B = 2.0 * (hj * uj - hk * uk);
+  const double C = (cj - ck) - hj * uj * uj + hk * uk * uk;
+  const double scale = fabs(hj) + fabs(hk);
+  if (fabs(A) <= 1e-13 * scale) {
+    if (B != 0.0) r0 = m0 - C / B;
+    if (A != 0.0) r1 = m0 - B / (2.0 * A);  // near-degenerate: also guard the vertex
+    return;
+  }
+  const double D = B * B - 4.0 * A * C;
+  if (D < 0.0) {
+    if (D > -1e-9 * B * B) r0 = m0 - B / (2.0 * A);  // near-tangent: guard the vertex
+    return;
+  }
+  const double sq = sqrt(D);
+  const double q = -0.5 * (B + copysign(sq, B));
+  if (q != 0.0) {
+    r0 = m0 + q / A;
+    r1 = m0 + C / q;
+  } else {
+    r0 = m0 - B / (2.0 * A);
+  }
+}
+
+template <int G>
+__device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int lane, BucketView bv, int maxit,
+                                  long long& passes_out) {
+  constexpr int NV = 3 * G + 1;
+  constexpr int P = G * (G - 1) / 2;
+  constexpr int KPL = kBuckets / 32;  // buckets per lane
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // ---- range of W_i ----------------------------------------------------------------
+  double mn = INFINITY, mx = -INFINITY;
+#pragma unroll 4
+  for (int s = lane; s < L; s += 32) {
+    const double v = (double)__ldg(A + s);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+#pragma unroll 1
+  for (int off = 16; off; off >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, off));
+  }
+  const double R = mx - mn;
+  if (!(R > 0.0) || G == 1) return 0.0;
+  const double bscale = (double)kBuckets / R;
+  // ---- stable counting sort of sample indices by value bucket ------------------------
+  for (int b = lane; b <= kBuckets; b += 32) bv.off[b] = 0;
+  __syncwarp();
+#pragma unroll 1
+  for (int s0 = 0; s0 < L; s0 += 32) {
+    const int s = s0 + lane;
+    int b = kBuckets;
+    if (s < L) {
+      b = (int)(((double)__ldg(A + s) - mn) * bscale);
+      b = b > kBuckets - 1 ? kBuckets - 1 : b;
+    }
+    const unsigned peers = __match_any_sync(FULL, b);
+    if (b < kBuckets && (peers & lt_mask) == 0) bv.off[b + 1] += (uint16_t)__popc(peers);
+    __syncwarp();
+  }
+  {
+    // exclusive prefix over buckets: lane owns KPL consecutive counters
+    int run = 0;
+    int loc[KPL];
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+      loc[q] = bv.off[lane * KPL + q + 1];
+      run += loc[q];
+    }
+    int incl = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += o;
+    }
+    int base = incl - run;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+      bv.off[lane * KPL + q] = (uint16_t)base;
+      bv.cur[lane * KPL + q] = (uint16_t)base;
+      base += loc[q];
+    }
+    if (lane == 31) bv.off[kBuckets] = (uint16_t)L;
+    __syncwarp();
+  }
+#pragma unroll 1
+  for (int s0 = 0; s0 < L; s0 += 32) {
+    const int s = s0 + lane;
+    int b = kBuckets;
+    if (s < L) {
+      b = (int)(((double)__ldg(A + s) - mn) * bscale);
+      b = b > kBuckets - 1 ? kBuckets - 1 : b;
+    }
+    const unsigned peers = __match_any_sync(FULL, b);
+    int base = 0;
+    if (b < kBuckets) {
+      base = bv.cur[b];
+      bv.pos[base + __popc(peers & lt_mask)] = (uint16_t)s;
+    }
+    __syncwarp();
+    if (b < kBuckets && (peers & lt_mask) == 0) bv.cur[b] = (uint16_t)(base + __popc(peers));
+    __syncwarp();
+  }
+  // ---- per-bucket range and shifted sums (one lane per bucket, slot order) ----------
+#pragma unroll 1
+  for (int q = 0; q < KPL; ++q) {
+    const int b = lane + 32 * q;
+    const int i0 = bv.off[b], i1 = bv.off[b + 1];
+    float lo = INFINITY, hi = -INFINITY, c = 0.f;
+    double a1 = 0.0, a2 = 0.0;
+    if (i1 > i0) {
+      c = __ldg(A + bv.pos[i0]);
+      for (int i = i0; i < i1; ++i) {
+        const float v = __ldg(A + bv.pos[i]);
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+        const double d = (double)v - (double)c;
+        a1 += d;
+        a2 += d * d;
+      }
+    }
+    bv.bmin[b] = lo;
+    bv.bmax[b] = hi;
+    bv.cb[b] = c;
+    bv.s1[b] = a1;
+    bv.s2[b] = a2;
+    bv.blab[b] = 0xFE;
+  }
+  __syncwarp();
+  // ---- CEM passes --------------------------------------------------------------------
+  Cem<G> cem;
+  cem.init(mn, R);
+  const double delta = 1e-6 * R;
+  int passes = 0;
+#pragma unroll 1
+  for (int it = 1; it <= maxit; ++it) {
+    // crossings of every live pair: lane p < P solves pair p, then broadcast
+    double rt[2 * (P > 0 ? P : 1)];
+    {
+      double r0 = NAN, r1 = NAN;
+      int pj = 0, pk = 1, cntp = 0;
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+#pragma unroll
+        for (int k = j + 1; k < G; ++k) {
+          if (cntp == lane) { pj = j; pk = k; }
+          ++cntp;
+        }
+      if (lane < P) {
+        double muj = 0, cj = 0, hj = 0, muk = 0, ck = 0, hk = 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (j == pj) { muj = cem.mu[j]; cj = cem.c[j]; hj = cem.h[j]; }
+          if (j == pk) { muk = cem.mu[j]; ck = cem.c[j]; hk = cem.h[j]; }
+        }
+        if (it == 1) { cj = ck = 0.0; hj = hk = 1.0; }  // first pass: argmin (y - mu)^2
+        score_crossings(muj, cj, hj, muk, ck, hk, mn, r0, r1);
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        rt[2 * p] = __shfl_sync(FULL, r0, p);
+        rt[2 * p + 1] = __shfl_sync(FULL, r1, p);
+      }
+    }
+    double v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    unsigned strad = 0, relab = 0;
+    int changed = 0;
+#pragma unroll 1
+    for (int q = 0; q < KPL; ++q) {
+      const int b = lane + 32 * q;
+      const int cnt = bv.off[b + 1] - bv.off[b];
+      if (cnt == 0) continue;
+      const double lo = (double)bv.bmin[b] - delta, hi = (double)bv.bmax[b] + delta;
+      bool st = false;
+#pragma unroll
+      for (int r = 0; r < 2 * P; ++r) st |= (rt[r] >= lo) & (rt[r] <= hi);
+      if (st) {
+        strad |= 1u << q;
+        bv.blab[b] = 0xFF;
+        continue;
+      }
+      double e[G];
+      const int lbl = cem.assign((double)bv.bmin[b], it, e);
+      const double c = (double)bv.cb[b], a1 = bv.s1[b], a2 = bv.s2[b], n = (double)cnt;
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (lbl == j) {
+          const double dc = c - cem.mu[j];
+          v[j] += n;
+          v[G + j] += n * c + a1;
+          v[2 * G + j] += a2 + dc * (2.0 * a1 + n * dc);
+        }
+      if (bv.blab[b] != lbl) {
+        relab |= 1u << q;
+        bv.blab[b] = (uint8_t)lbl;
+      }
+    }
+    __syncwarp();
+    // members of straddling buckets (per sample) and of relabelled buckets
+    unsigned todo = __ballot_sync(FULL, (strad | relab) != 0);
+#pragma unroll 1
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const unsigned ms = __shfl_sync(FULL, strad, src), mr = __shfl_sync(FULL, relab, src);
+      unsigned m = ms | mr;
+#pragma unroll 1
+      while (m) {
+        const int q = __ffs(m) - 1;
+        m &= m - 1;
+        const int b = src + 32 * q;
+        const int i0 = bv.off[b], i1 = bv.off[b + 1];
+        const bool per_sample = (ms >> q) & 1u;
+        const int wl = bv.blab[b];
+#pragma unroll 1
+        for (int i = i0 + lane; i < i1; i += 32) {
+          int lbl = wl;
+          if (per_sample) {
+            const double y = (double)__ldg(A + bv.pos[i]);
+            double e[G];
+            lbl = cem.assign(y, it, e);
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+              if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
+          }
+          changed |= (int)(bv.lab[i] != lbl);
+          bv.lab[i] = (uint8_t)lbl;
+        }
+      }
+    }
+    __syncwarp();
+    v[3 * G] = (double)changed;
+    xor_sum_vec<NV>(v, 32);
+    passes = it;
+    if ((it > 1 && v[3 * G] == 0.0) || it == maxit) break;  // labels final
+    mstep<G>(cem, v, L, 32, lane);
+  }
+  // ---- final groups on W_i and the same index sets on W_{i+1} (slot order, Z28) -----
+  double w[NV];  // nA[G], SA[G], SB[G], TB ; TA separately (same order)
+#pragma unroll
+  for (int i = 0; i < NV; ++i) w[i] = 0.0;
+  double TA = 0.0;
+  const float* B = A + L;
+#pragma unroll 2
+  for (int i = lane; i < L; i += 32) {
+    const int p = bv.pos[i];
+    const double ya = (double)__ldg(A + p), yb = (double)__ldg(B + p);
+    TA += ya;
+    w[3 * G] += yb;
+    const int l = bv.lab[i];
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      if (l == j) { w[j] += 1.0; w[G + j] += ya; w[2 * G + j] += yb; }
+  }
+  xor_sum_vec<NV>(w, 32);
+#pragma unroll 1
+  for (int off = 16; off; off >>= 1) TA += __shfl_xor_sync(FULL, TA, off);
+  if (lane == 0) passes_out += (long long)(passes + 1) * L;
+  const double mA = TA / (double)L, mB = w[3 * G] / (double)L;
+  double num = 0.0;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    if (w[j] == 0.0) continue;
+    num += w[j] * smape(w[G + j] / w[j] - mA, w[2 * G + j] / w[j] - mB);
+  }
+  return num / (double)L;
+}
+
+// ---------------------------------------------------------------------------------
 // Streaming warp mode (L > kRegMaxL): one warp per pair; samples re-read from L1/L2.
 template <int G>
 __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane, uint8_t* lab, int maxit,
@@ -422,7 +767,7 @@ struct ScoreArgs {
   double* err_out;
   uint8_t* lab_scratch;  // [gridDim][8 warps][lab_stride] when L > lab_cap
   int32_t lab_stride;
-  int32_t lab_cap;       // bytes of smem labels per warp (streaming mode)
+  int32_t bucket_lcap;   // bucket path handles kBucketMinL <= L <= bucket_lcap
   unsigned long long* cem_ctr;
 };
 
@@ -431,8 +776,9 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(
   __shared__ int64_t s_item;
   __shared__ double s_team[kScoreThreads];
   __shared__ double s_red[2 * kWarps * 32];
-  __shared__ double s_ys[kLpt * kScoreThreads];  // register-path samples, [u][thread]
-  extern __shared__ uint8_t s_lab[];  // [8 warps][lab_cap] (streaming mode, L <= lab_cap)
+  // dynamic: team path samples double[kLpt][256] | bucket path 8 x BucketView regions
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  double* s_ys = reinterpret_cast<double*>(s_dyn);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long total = *a.count;
   long long passes = 0;
@@ -451,7 +797,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(
     const float* yt = a.y + t * (int64_t)a.N;
     double acc = 0.0;
     int tau;
-    if (L <= kRegMaxL) {
+    if (L < kBucketMinL) {
       tau = 1;
       while (tau * kLpt < L) tau <<= 1;
       const int nteams = kScoreThreads / tau;
@@ -469,10 +815,17 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(
         if (has) acc += e;
       }
       if (lt != 0) acc = 0.0;
+    } else if (L <= a.bucket_lcap) {
+      tau = 32;
+      BucketView bv = BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap), a.bucket_lcap);
+      for (int pidx = warp; pidx < npairs; pidx += kWarps) {
+        acc += pair_err_bucket<G>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes);
+        __syncwarp();
+      }
+      if (lane != 0) acc = 0.0;
     } else {
       tau = 32;
-      uint8_t* lab = (L <= a.lab_cap) ? s_lab + (int64_t)warp * a.lab_cap
-                                      : a.lab_scratch + ((int64_t)blockIdx.x * kWarps + warp) * a.lab_stride;
+      uint8_t* lab = a.lab_scratch + ((int64_t)blockIdx.x * kWarps + warp) * a.lab_stride;
       for (int pidx = warp; pidx < npairs; pidx += kWarps) {
         acc += pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
         __syncwarp();
@@ -503,32 +856,37 @@ static int grid_for(size_t smem) {
   return sms * occ < kMaxScoreCtas ? sms * occ : kMaxScoreCtas;
 }
 
-static size_t score_smem(int32_t max_L, int32_t* lab_cap) {
+static size_t score_smem(int32_t max_L, int32_t* bucket_lcap) {
   int32_t cap = 0;
-  if (max_L > kRegMaxL) cap = ((max_L < kLabCap ? max_L : kLabCap) + 15) & ~15;
-  if (lab_cap) *lab_cap = cap;
-  return (size_t)cap * kWarps;
+  size_t bytes = (size_t)kLpt * kScoreThreads * sizeof(double);  // team path
+  if (max_L >= kBucketMinL) {
+    cap = ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15;
+    const size_t b = (size_t)kWarps * bucket_region_bytes(cap);
+    if (b > bytes) bytes = b;
+  }
+  if (bucket_lcap) *bucket_lcap = cap;
+  return bytes;
 }
 
 int score_grid(int G) {
   switch (G) {
-    case 1: return grid_for<1>(0);
-    case 2: return grid_for<2>(0);
-    case 3: return grid_for<3>(0);
-    case 4: return grid_for<4>(0);
-    case 5: return grid_for<5>(0);
-    case 6: return grid_for<6>(0);
-    case 7: return grid_for<7>(0);
-    default: return grid_for<8>(0);
+    case 1: return grid_for<1>(score_smem(1 << 17, nullptr));
+    case 2: return grid_for<2>(score_smem(1 << 17, nullptr));
+    case 3: return grid_for<3>(score_smem(1 << 17, nullptr));
+    case 4: return grid_for<4>(score_smem(1 << 17, nullptr));
+    case 5: return grid_for<5>(score_smem(1 << 17, nullptr));
+    case 6: return grid_for<6>(score_smem(1 << 17, nullptr));
+    case 7: return grid_for<7>(score_smem(1 << 17, nullptr));
+    default: return grid_for<8>(score_smem(1 << 17, nullptr));
   }
 }
 
 cudaError_t launch_score(const Plan& p, const float* y, const int4* items, const unsigned long long* count,
                          unsigned long long* cursor, double* err_out, uint8_t* lab_scratch, int32_t lab_stride,
                          unsigned long long* cem_ctr, int32_t max_L, cudaStream_t s) {
-  int32_t lab_cap = 0;
-  const size_t smem = score_smem(max_L, &lab_cap);
-  ScoreArgs a{y, p.N, p.maxit, items, count, cursor, err_out, lab_scratch, lab_stride, lab_cap, cem_ctr};
+  int32_t bucket_lcap = 0;
+  const size_t smem = score_smem(max_L, &bucket_lcap);
+  ScoreArgs a{y, p.N, p.maxit, items, count, cursor, err_out, lab_scratch, lab_stride, bucket_lcap, cem_ctr};
 #define GPOEO_SCORE_CASE(GG)                                                                              \
   case GG: {                                                                                            \
     cudaError_t e = cudaFuncSetAttribute(score_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
