@@ -141,11 +141,12 @@ Work carve(const Plan& pl, const Layout& L, void* ws) {
   w.local_lo = reinterpret_cast<int32_t*>(b + L.off_llo);
   w.local_hi = reinterpret_cast<int32_t*>(b + L.off_lhi);
   w.local_base = reinterpret_cast<int64_t*>(b + L.off_lbase);
-  w.items_a = reinterpret_cast<int4*>(b + L.off_ia);
-  w.items_b = reinterpret_cast<int4*>(b + L.off_ib);
+  w.list_a = ItemList{reinterpret_cast<int4*>(b + L.off_ia), (int64_t)pl.batch * pl.K, &w.ctr[CTR_A_SMALL],
+                      &w.ctr[CTR_A_BIG], &w.ctr[CTR_CUR_A_SMALL], &w.ctr[CTR_CUR_A_BIG]};
+  w.list_b = ItemList{reinterpret_cast<int4*>(b + L.off_ib), (int64_t)pl.batch * pl.max_local, &w.ctr[CTR_B_SMALL],
+                      &w.ctr[CTR_B_BIG], &w.ctr[CTR_CUR_B_SMALL], &w.ctr[CTR_CUR_B_BIG]};
   w.local_err = reinterpret_cast<double*>(b + L.off_lerr);
   w.lab_scratch = L.lab_stride ? reinterpret_cast<uint8_t*>(b + L.off_lab) : nullptr;
-  (void)pl;
   return w;
 }
 
@@ -177,14 +178,14 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   if (pl.batch > 0) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
   CK(mark(2));
   if (pl.batch > 0)
-    CK(launch_score(pl, w.y, w.items_a, &w.ctr[CTR_ITEMS_A], &w.ctr[CTR_CURSOR_A], w.cand_err, w.lab_scratch,
-                    L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
+    CK(launch_score(pl, w.y, w.list_a, w.cand_err, w.lab_scratch, L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmin,
+                    pl.Lmax, s));
   CK(mark(3));
   if (pl.batch > 0) CK(launch_select(pl, w, s));
   CK(mark(4));
   if (pl.batch > 0)
-    CK(launch_score(pl, w.y, w.items_b, &w.ctr[CTR_ITEMS_B], &w.ctr[CTR_CURSOR_B], w.local_err, w.lab_scratch,
-                    L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmax, s));
+    CK(launch_score(pl, w.y, w.list_b, w.local_err, w.lab_scratch, L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmin,
+                    pl.Lmax, s));
   CK(mark(5));
   if (pl.batch > 0) CK(launch_final(pl, w, results, detail, s));
   CK(mark(6));
@@ -193,12 +194,11 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// pack (trace_index, period) into scorer items; count = n
+// pack (trace_index, period) into a two-ended scorer list
 __global__ void pack_items_kernel(const int32_t* __restrict__ ti, const int32_t* __restrict__ per, int64_t n,
-                                  int4* __restrict__ items, unsigned long long* ctr) {
+                                  ItemList list) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0) ctr[CTR_ITEMS_A] = (unsigned long long)n;
-  if (i < n) items[i] = make_int4(ti[i], per[i], (int)i, 0);
+  if (i < n) append_item(list, ti[i], per[i], (int)i);
 }
 
 }  // namespace
@@ -385,12 +385,12 @@ int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples
   pl.G = num_groups;
   pl.maxit = gmm_max_iters;
   pl.batch = batch;
+  ItemList list{items, n_queries, &ctr[CTR_A_SMALL], &ctr[CTR_A_BIG], &ctr[CTR_CUR_A_SMALL], &ctr[CTR_CUR_A_BIG]};
   CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
-  pack_items_kernel<<<(unsigned)((n_queries + 255) / 256), 256, 0, s>>>(trace_index, period, n_queries, items, ctr);
+  pack_items_kernel<<<(unsigned)((n_queries + 255) / 256), 256, 0, s>>>(trace_index, period, n_queries, list);
   CK(cudaGetLastError());
   const int32_t maxL = n_samples / 2;
-  CK(launch_score(pl, signal, items, &ctr[CTR_ITEMS_A], &ctr[CTR_CURSOR_A], error_out, lab,
-                  ((maxL + 15) & ~15), &ctr[CTR_CEM_PASSES], maxL, s));
+  CK(launch_score(pl, signal, list, error_out, lab, ((maxL + 15) & ~15), &ctr[CTR_CEM_PASSES], 2, maxL, s));
   return GPOEO_OK;
 }
 
@@ -403,8 +403,8 @@ int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t ba
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaMemcpyAsync(h, workspace, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess) return GPOEO_ERR_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return GPOEO_ERR_CUDA;
-  out->n_candidate_queries = (int64_t)h[CTR_ITEMS_A];
-  out->n_local_queries = (int64_t)h[CTR_ITEMS_B];
+  out->n_candidate_queries = (int64_t)(h[CTR_A_SMALL] + h[CTR_A_BIG]);
+  out->n_local_queries = (int64_t)(h[CTR_B_SMALL] + h[CTR_B_BIG]);
   out->cem_sample_passes = (int64_t)h[CTR_CEM_PASSES];
   return GPOEO_OK;
 }

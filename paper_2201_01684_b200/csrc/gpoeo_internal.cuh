@@ -30,6 +30,54 @@ struct Plan {
   int64_t batch;
 };
 
+enum CounterSlot {
+  CTR_A_SMALL = 0,     // candidate queries with L < kBucketMinL (front of items_a)
+  CTR_A_BIG = 1,       // candidate queries with L >= kBucketMinL (back of items_a)
+  CTR_B_SMALL = 2,     // local queries, front of items_b
+  CTR_B_BIG = 3,       // local queries, back of items_b
+  CTR_CUR_A_SMALL = 4, // persistent-scheduler cursors
+  CTR_CUR_A_BIG = 5,
+  CTR_CUR_B_SMALL = 6,
+  CTR_CUR_B_BIG = 7,
+  CTR_CEM_PASSES = 8,  // sum of CEM sample passes (work counter)
+  CTR_LOCAL_SLOTS = 9, // local-score slots handed out by select
+};
+
+constexpr int kBucketMinL = 257;  // L >= this: bucketed warp path (score.cu)
+
+// A query list: small-L items packed from the front, the others from the back, so the
+// two scorer kernels (team path / bucketed path) each read one contiguous range.
+struct ItemList {
+  int4* items;
+  int64_t cap;
+  unsigned long long* n_small;
+  unsigned long long* n_big;
+  unsigned long long* cur_small;
+  unsigned long long* cur_big;
+};
+
+__device__ __forceinline__ void append_items(const ItemList& l, int t, int L0, int count, int slot0) {
+  // items (t, L0 + i, slot0 + i), i < count; L increasing
+  int ns = 0;
+  while (ns < count && L0 + ns < kBucketMinL) ++ns;
+  if (ns) {
+    const unsigned long long b = atomicAdd(l.n_small, (unsigned long long)ns);
+    for (int i = 0; i < ns; ++i) l.items[b + i] = make_int4(t, L0 + i, slot0 + i, 0);
+  }
+  if (count - ns) {
+    const unsigned long long b = atomicAdd(l.n_big, (unsigned long long)(count - ns));
+    for (int i = ns; i < count; ++i) l.items[l.cap - 1 - (int64_t)(b + (i - ns))] = make_int4(t, L0 + i, slot0 + i, 0);
+  }
+}
+
+__device__ __forceinline__ void append_item(const ItemList& l, int t, int L, int slot) {
+  if (L < kBucketMinL) {
+    l.items[atomicAdd(l.n_small, 1ull)] = make_int4(t, L, slot, 0);
+  } else {
+    l.items[l.cap - 1 - (int64_t)atomicAdd(l.n_big, 1ull)] = make_int4(t, L, slot, 0);
+  }
+}
+
 // Device pointers carved out of the caller's workspace (gpoeo_api.cu: carve()).
 struct Work {
   float* y;                 // [B][N] composite signal
@@ -43,31 +91,21 @@ struct Work {
   int32_t* local_lo;        // [B]
   int32_t* local_hi;        // [B]
   int64_t* local_base;      // [B]
-  int4* items_a;            // [B*K]   candidate queries (trace, L, out slot, -)
-  int4* items_b;            // [B*max_local] local queries
+  ItemList list_a;          // [B*K]   candidate queries (trace, L, out slot, -)
+  ItemList list_b;          // [B*max_local] local queries
   double* local_err;        // [B*max_local]
   uint8_t* lab_scratch;     // warp-mode label scratch for L > kLabCap (may be null)
   unsigned long long* ctr;  // [kCounterSlots]
-};
-
-enum CounterSlot {
-  CTR_ITEMS_A = 0,     // number of candidate queries appended
-  CTR_ITEMS_B = 1,     // number of local queries appended
-  CTR_CURSOR_A = 2,    // persistent-scheduler cursors
-  CTR_CURSOR_B = 3,
-  CTR_CEM_PASSES = 4,  // sum of CEM sample passes (work counter)
 };
 
 // Launchers (each returns cudaGetLastError()).
 cudaError_t launch_composite(const float* x, const Plan& p, float* y, int32_t* status, cudaStream_t s);
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
                             bool find_peaks, cudaStream_t s);
-cudaError_t launch_score(const Plan& p, const float* y, const int4* items, const unsigned long long* count,
-                         unsigned long long* cursor, double* err_out, uint8_t* lab_scratch, int32_t lab_stride,
-                         unsigned long long* cem_ctr, int32_t max_L, cudaStream_t s);
+cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
+                         int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);
 cudaError_t launch_final(const Plan& p, Work w, gpoeo_result* results, gpoeo_detail* detail, cudaStream_t s);
 
-int score_grid(int G);  // persistent grid size of the scorer
 
 }  // namespace gpoeo

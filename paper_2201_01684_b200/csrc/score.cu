@@ -350,31 +350,32 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 // per-sample rule gives at the bucket minimum, and its statistics come from the bucket
 // sums (sum (y - mu)^2 = S2 + (c - mu)(2 S1 + n (c - mu)), no cancellation). Members of
 // the few buckets that straddle a root (delta = 1e-6 R absorbs root rounding) are
-// evaluated one by one with exactly the per-sample rule of the register path. Labels are
-// kept per sorted slot so "no label changed" is exact. The final W_i / W_{i+1} pass walks
-// the slots in one order for both windows (Z28). Decisions equal the per-sample
-// evaluation except at sub-rounding margins (Z27). Cost per pass: O(K + straddled
-// samples) instead of O(L).
-constexpr int kBuckets = 128;
-constexpr int kBucketMinL = kLpt * 16 + 1;  // 257: above this the pair is bucketed
+// evaluated one by one with exactly the per-sample rule of the register path, in one
+// flattened sweep over all straddling members. Labels are kept per sorted slot so "no
+// label changed" is exact. The final W_i / W_{i+1} pass walks the slots in one order for
+// both windows (Z28). Decisions equal the per-sample evaluation except at sub-rounding
+// margins (Z27). Cost per pass: O(K + straddled samples) instead of O(L).
+constexpr int kBuckets = 64;
 constexpr int kBucketMaxL = 8192;
+constexpr int kBucketWarps = 4;  // bucket-kernel CTA: 4 warps, one pair each
 
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
-  return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) +
-         (size_t)(kBuckets + 1) * 2 + 14 + (size_t)kBuckets * 2 + (size_t)kBuckets * 4 * 3 + (size_t)kBuckets * 8 * 2 +
+  return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) + (size_t)kBuckets * 8 * 2 +
+         (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 2 + (size_t)kBuckets * 4 +
          kBuckets + 64;
 }
 
 struct BucketView {
   uint16_t* pos;   // [Lcap] sorted slot -> sample index in the window
   uint8_t* lab;    // [Lcap] label of each sorted slot
-  uint16_t* off;   // [K+1] first slot of bucket b
-  uint16_t* cur;   // [K]   scatter cursors
+  double* s1;      // [K]   sum (y - c_b)
+  double* s2;      // [K]   sum (y - c_b)^2
   float* bmin;     // [K]
   float* bmax;     // [K]
   float* cb;       // [K]   shift (first member's value)
-  double* s1;      // [K]   sum (y - c_b)
-  double* s2;      // [K]   sum (y - c_b)^2
+  uint16_t* off;   // [K+1] first slot of bucket b
+  uint16_t* cur;   // [K]   scatter cursors
+  uint32_t* flag;  // [K]   flagged-bucket list of a pass: (member offset << 8) | bucket
   uint8_t* blab;   // [K]   whole-bucket label, 0xFF per-sample, 0xFE unset
 
   __device__ static BucketView carve(uint8_t* base, int Lcap) {
@@ -395,9 +396,11 @@ struct BucketView {
     v.cb = reinterpret_cast<float*>(p);
     p += (size_t)kBuckets * 4;
     v.off = reinterpret_cast<uint16_t*>(p);
-    p += (size_t)(kBuckets + 1) * 2 + 14;
+    p += (size_t)(kBuckets + 8) * 2;
     v.cur = reinterpret_cast<uint16_t*>(p);
     p += (size_t)kBuckets * 2;
+    v.flag = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)kBuckets * 4;
     v.blab = p;
     return v;
   }
@@ -473,8 +476,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   }
   {
     // exclusive prefix over buckets: lane owns KPL consecutive counters
-    int run = 0;
     int loc[KPL];
+    int run = 0;
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
       loc[q] = bv.off[lane * KPL + q + 1];
@@ -524,6 +527,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     double a1 = 0.0, a2 = 0.0;
     if (i1 > i0) {
       c = __ldg(A + bv.pos[i0]);
+#pragma unroll 4
       for (int i = i0; i < i1; ++i) {
         const float v = __ldg(A + bv.pos[i]);
         lo = fminf(lo, v);
@@ -545,6 +549,18 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   Cem<G> cem;
   cem.init(mn, R);
   const double delta = 1e-6 * R;
+  // pair of components solved by this lane (lane < P)
+  int pj = 0, pk = 1;
+  {
+    int cntp = 0;
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+#pragma unroll
+      for (int k = j + 1; k < G; ++k) {
+        if (cntp == lane) { pj = j; pk = k; }
+        ++cntp;
+      }
+  }
   int passes = 0;
 #pragma unroll 1
   for (int it = 1; it <= maxit; ++it) {
@@ -552,14 +568,6 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     double rt[2 * (P > 0 ? P : 1)];
     {
       double r0 = NAN, r1 = NAN;
-      int pj = 0, pk = 1, cntp = 0;
-#pragma unroll
-      for (int j = 0; j < G; ++j)
-#pragma unroll
-        for (int k = j + 1; k < G; ++k) {
-          if (cntp == lane) { pj = j; pk = k; }
-          ++cntp;
-        }
       if (lane < P) {
         double muj = 0, cj = 0, hj = 0, muk = 0, ck = 0, hk = 0;
 #pragma unroll
@@ -579,11 +587,12 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;
-    unsigned strad = 0, relab = 0;
-    int changed = 0;
-#pragma unroll 1
+    // classify this lane's buckets; count members that need per-slot work
+    int need[KPL];
+#pragma unroll
     for (int q = 0; q < KPL; ++q) {
       const int b = lane + 32 * q;
+      need[q] = 0;
       const int cnt = bv.off[b + 1] - bv.off[b];
       if (cnt == 0) continue;
       const double lo = (double)bv.bmin[b] - delta, hi = (double)bv.bmax[b] + delta;
@@ -591,8 +600,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
 #pragma unroll
       for (int r = 0; r < 2 * P; ++r) st |= (rt[r] >= lo) & (rt[r] <= hi);
       if (st) {
-        strad |= 1u << q;
         bv.blab[b] = 0xFF;
+        need[q] = cnt;
         continue;
       }
       double e[G];
@@ -607,41 +616,66 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
           v[2 * G + j] += a2 + dc * (2.0 * a1 + n * dc);
         }
       if (bv.blab[b] != lbl) {
-        relab |= 1u << q;
         bv.blab[b] = (uint8_t)lbl;
+        need[q] = cnt;
       }
     }
-    __syncwarp();
-    // members of straddling buckets (per sample) and of relabelled buckets
-    unsigned todo = __ballot_sync(FULL, (strad | relab) != 0);
-#pragma unroll 1
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const unsigned ms = __shfl_sync(FULL, strad, src), mr = __shfl_sync(FULL, relab, src);
-      unsigned m = ms | mr;
-#pragma unroll 1
-      while (m) {
-        const int q = __ffs(m) - 1;
-        m &= m - 1;
-        const int b = src + 32 * q;
-        const int i0 = bv.off[b], i1 = bv.off[b + 1];
-        const bool per_sample = (ms >> q) & 1u;
-        const int wl = bv.blab[b];
-#pragma unroll 1
-        for (int i = i0 + lane; i < i1; i += 32) {
-          int lbl = wl;
-          if (per_sample) {
-            const double y = (double)__ldg(A + bv.pos[i]);
-            double e[G];
-            lbl = cem.assign(y, it, e);
+    // flattened list of flagged buckets: (exclusive member offset << 8) | bucket
+    int mine = 0;
 #pragma unroll
-            for (int j = 0; j < G; ++j)
-              if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
+    for (int q = 0; q < KPL; ++q) mine += need[q];
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += o;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    int changed = 0;
+    if (total) {
+      // compact flagged buckets in (lane, q) order
+      int myfl = 0;
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) myfl += need[q] != 0;
+      int fi = myfl;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(FULL, fi, off);
+        if (lane >= off) fi += o;
+      }
+      const int nfl = __shfl_sync(FULL, fi, 31);
+      {
+        int mo = incl - mine, k = fi - myfl;
+#pragma unroll
+        for (int q = 0; q < KPL; ++q)
+          if (need[q]) {
+            bv.flag[k++] = ((uint32_t)mo << 8) | (uint32_t)(lane + 32 * q);
+            mo += need[q];
           }
-          changed |= (int)(bv.lab[i] != lbl);
-          bv.lab[i] = (uint8_t)lbl;
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int g = lane; g < total; g += 32) {
+        // bucket of flattened member g: last flag with offset <= g
+        int lo = 0, hi = nfl - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if ((int)(bv.flag[mid] >> 8) <= g) lo = mid; else hi = mid - 1;
         }
+        const uint32_t f = bv.flag[lo];
+        const int b = (int)(f & 0xFFu);
+        const int i = bv.off[b] + (g - (int)(f >> 8));
+        int lbl = bv.blab[b];
+        if (lbl == 0xFF) {
+          const double y = (double)__ldg(A + bv.pos[i]);
+          double e[G];
+          lbl = cem.assign(y, it, e);
+#pragma unroll
+          for (int j = 0; j < G; ++j)
+            if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
+        }
+        changed |= (int)(bv.lab[i] != lbl);
+        bv.lab[i] = (uint8_t)lbl;
       }
     }
     __syncwarp();
@@ -761,24 +795,29 @@ struct ScoreArgs {
   const float* y;
   int32_t N;
   int32_t maxit;
-  const int4* items;
+  const int4* items;   // list base
+  int64_t cap;         // list capacity (big items are stored from the back)
   const unsigned long long* count;
   unsigned long long* cursor;
+  int reverse;         // 1: item k is items[cap - 1 - k]
   double* err_out;
-  uint8_t* lab_scratch;  // [gridDim][8 warps][lab_stride] when L > lab_cap
+  uint8_t* lab_scratch;  // [gridDim][warps][lab_stride] streaming path (L > bucket_lcap)
   int32_t lab_stride;
   int32_t bucket_lcap;   // bucket path handles kBucketMinL <= L <= bucket_lcap
   unsigned long long* cem_ctr;
 };
 
+__device__ __forceinline__ int4 fetch_item(const ScoreArgs& a, int64_t k) {
+  return a.items[a.reverse ? a.cap - 1 - k : k];
+}
+
+// Team path (L < kBucketMinL): 256 threads, one query at a time, teams of tau lanes.
 template <int G>
-__global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_kernel(ScoreArgs a) {
   __shared__ int64_t s_item;
   __shared__ double s_team[kScoreThreads];
   __shared__ double s_red[2 * kWarps * 32];
-  // dynamic: team path samples double[kLpt][256] | bucket path 8 x BucketView regions
-  extern __shared__ __align__(16) uint8_t s_dyn[];
-  double* s_ys = reinterpret_cast<double*>(s_dyn);
+  __shared__ double s_ys[kLpt * kScoreThreads];  // samples, [u][thread]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long total = *a.count;
   long long passes = 0;
@@ -790,48 +829,28 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(
     __syncthreads();
     if ((unsigned long long)item >= total) break;
     buf = 0;  // teams are re-formed per query: every warp restarts the reduction parity
-    const int4 q = a.items[item];
+    const int4 q = fetch_item(a, item);
     const int64_t t = q.x;
     const int32_t L = q.y;
     const int32_t npairs = a.N / L - 1;
     const float* yt = a.y + t * (int64_t)a.N;
     double acc = 0.0;
-    int tau;
-    if (L < kBucketMinL) {
-      tau = 1;
-      while (tau * kLpt < L) tau <<= 1;
-      const int nteams = kScoreThreads / tau;
-      const int team = tid / tau;
-      const int lt = tid & (tau - 1);
-      // warp-uniform trip count (sub-warp teams of one warp: team0 .. team0 + 32/tau - 1)
-      const int team0 = tau >= 32 ? team : (warp * 32) / tau;
-      const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
-      for (int i = 0; i < trips; ++i) {
-        const int pidx = team + i * nteams;
-        const bool has = pidx < npairs;
-        const float* A = yt + (int64_t)(has ? pidx : 0) * L;
-        const double e =
-            pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
-        if (has) acc += e;
-      }
-      if (lt != 0) acc = 0.0;
-    } else if (L <= a.bucket_lcap) {
-      tau = 32;
-      BucketView bv = BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap), a.bucket_lcap);
-      for (int pidx = warp; pidx < npairs; pidx += kWarps) {
-        acc += pair_err_bucket<G>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes);
-        __syncwarp();
-      }
-      if (lane != 0) acc = 0.0;
-    } else {
-      tau = 32;
-      uint8_t* lab = a.lab_scratch + ((int64_t)blockIdx.x * kWarps + warp) * a.lab_stride;
-      for (int pidx = warp; pidx < npairs; pidx += kWarps) {
-        acc += pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
-        __syncwarp();
-      }
-      if (lane != 0) acc = 0.0;
+    int tau = 1;
+    while (tau * kLpt < L) tau <<= 1;
+    const int nteams = kScoreThreads / tau;
+    const int team = tid / tau;
+    const int lt = tid & (tau - 1);
+    // warp-uniform trip count (sub-warp teams of one warp: team0 .. team0 + 32/tau - 1)
+    const int team0 = tau >= 32 ? team : (warp * 32) / tau;
+    const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
+    for (int i = 0; i < trips; ++i) {
+      const int pidx = team + i * nteams;
+      const bool has = pidx < npairs;
+      const float* A = yt + (int64_t)(has ? pidx : 0) * L;
+      const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
+      if (has) acc += e;
     }
+    if (lt != 0) acc = 0.0;
     // per-team partials -> Err(L), in team order
     s_team[tid] = acc;
     __syncthreads();
@@ -846,68 +865,124 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_kernel(
   if (lane == 0 && passes) atomicAdd(a.cem_ctr, (unsigned long long)passes);
 }
 
+// Bucket path (L >= kBucketMinL): kBucketWarps warps per CTA, one query per CTA at a
+// time, one pair per warp at a time (streaming path beyond bucket_lcap).
 template <int G>
-static int grid_for(size_t smem) {
-  int dev = 0, sms = 148, occ = 1;
+__global__ void __launch_bounds__(kBucketWarps * 32) score_bucket_kernel(ScoreArgs a) {
+  __shared__ int64_t s_item;
+  __shared__ double s_team[kBucketWarps];
+  extern __shared__ __align__(16) uint8_t s_dyn[];  // kBucketWarps x BucketView regions
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long total = *a.count;
+  long long passes = 0;
+  for (;;) {
+    if (tid == 0) s_item = (int64_t)atomicAdd(a.cursor, 1ull);
+    __syncthreads();
+    const int64_t item = s_item;
+    __syncthreads();
+    if ((unsigned long long)item >= total) break;
+    const int4 q = fetch_item(a, item);
+    const int64_t t = q.x;
+    const int32_t L = q.y;
+    const int32_t npairs = a.N / L - 1;
+    const float* yt = a.y + t * (int64_t)a.N;
+    double acc = 0.0;
+    if (L <= a.bucket_lcap) {
+      BucketView bv = BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap), a.bucket_lcap);
+      for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
+        acc += pair_err_bucket<G>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes);
+        __syncwarp();
+      }
+    } else {
+      uint8_t* lab = a.lab_scratch + ((int64_t)blockIdx.x * kBucketWarps + warp) * a.lab_stride;
+      for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
+        acc += pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
+        __syncwarp();
+      }
+    }
+    if (lane == 0) s_team[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < kBucketWarps; ++w) sum += s_team[w];
+      a.err_out[q.z] = sum / (double)npairs;
+    }
+    __syncthreads();
+  }
+  for (int off = 16; off; off >>= 1) passes += __shfl_xor_sync(FULL, passes, off);
+  if (lane == 0 && passes) atomicAdd(a.cem_ctr, (unsigned long long)passes);
+}
+
+static int device_sms() {
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, score_kernel<G>, kScoreThreads, smem);
+  return sms;
+}
+
+template <typename K>
+static int grid_of(K kern, int threads, size_t smem) {
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (occ < 1) occ = 1;
-  return sms * occ < kMaxScoreCtas ? sms * occ : kMaxScoreCtas;
+  const int g = device_sms() * occ;
+  return g < kMaxScoreCtas ? g : kMaxScoreCtas;
 }
 
-static size_t score_smem(int32_t max_L, int32_t* bucket_lcap) {
-  int32_t cap = 0;
-  size_t bytes = (size_t)kLpt * kScoreThreads * sizeof(double);  // team path
+template <int G>
+static cudaError_t launch_g(const ScoreArgs& base, const ItemList& list, int32_t min_L, int32_t max_L,
+                            cudaStream_t s) {
+  if (min_L < kBucketMinL) {
+    ScoreArgs a = base;
+    a.count = list.n_small;
+    a.cursor = list.cur_small;
+    a.reverse = 0;
+    auto kern = score_team_kernel<G>;
+    score_team_kernel<G><<<grid_of(kern, kScoreThreads, 0), kScoreThreads, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   if (max_L >= kBucketMinL) {
-    cap = ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15;
-    const size_t b = (size_t)kWarps * bucket_region_bytes(cap);
-    if (b > bytes) bytes = b;
+    ScoreArgs a = base;
+    a.count = list.n_big;
+    a.cursor = list.cur_big;
+    a.reverse = 1;
+    const int lcap = ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15;
+    a.bucket_lcap = lcap;
+    const size_t smem = (size_t)kBucketWarps * bucket_region_bytes(lcap);
+    auto kern = score_bucket_kernel<G>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    score_bucket_kernel<G><<<grid_of(kern, kBucketWarps * 32, smem), kBucketWarps * 32, smem, s>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
-  if (bucket_lcap) *bucket_lcap = cap;
-  return bytes;
+  return cudaSuccess;
 }
 
-int score_grid(int G) {
-  switch (G) {
-    case 1: return grid_for<1>(score_smem(1 << 17, nullptr));
-    case 2: return grid_for<2>(score_smem(1 << 17, nullptr));
-    case 3: return grid_for<3>(score_smem(1 << 17, nullptr));
-    case 4: return grid_for<4>(score_smem(1 << 17, nullptr));
-    case 5: return grid_for<5>(score_smem(1 << 17, nullptr));
-    case 6: return grid_for<6>(score_smem(1 << 17, nullptr));
-    case 7: return grid_for<7>(score_smem(1 << 17, nullptr));
-    default: return grid_for<8>(score_smem(1 << 17, nullptr));
-  }
-}
-
-cudaError_t launch_score(const Plan& p, const float* y, const int4* items, const unsigned long long* count,
-                         unsigned long long* cursor, double* err_out, uint8_t* lab_scratch, int32_t lab_stride,
-                         unsigned long long* cem_ctr, int32_t max_L, cudaStream_t s) {
-  int32_t bucket_lcap = 0;
-  const size_t smem = score_smem(max_L, &bucket_lcap);
-  ScoreArgs a{y, p.N, p.maxit, items, count, cursor, err_out, lab_scratch, lab_stride, bucket_lcap, cem_ctr};
-#define GPOEO_SCORE_CASE(GG)                                                                              \
-  case GG: {                                                                                            \
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                         (int)smem);                                                    \
-    if (e != cudaSuccess) return e;                                                                     \
-    score_kernel<GG><<<grid_for<GG>(smem), kScoreThreads, smem, s>>>(a);                                \
-    break;                                                                                              \
-  }
+cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
+                         int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s) {
+  ScoreArgs a{};
+  a.y = y;
+  a.N = p.N;
+  a.maxit = p.maxit;
+  a.items = list.items;
+  a.cap = list.cap;
+  a.err_out = err_out;
+  a.lab_scratch = lab_scratch;
+  a.lab_stride = lab_stride;
+  a.cem_ctr = cem_ctr;
   switch (p.G) {
-    GPOEO_SCORE_CASE(1)
-    GPOEO_SCORE_CASE(2)
-    GPOEO_SCORE_CASE(3)
-    GPOEO_SCORE_CASE(4)
-    GPOEO_SCORE_CASE(5)
-    GPOEO_SCORE_CASE(6)
-    GPOEO_SCORE_CASE(7)
-    GPOEO_SCORE_CASE(8)
+    case 1: return launch_g<1>(a, list, min_L, max_L, s);
+    case 2: return launch_g<2>(a, list, min_L, max_L, s);
+    case 3: return launch_g<3>(a, list, min_L, max_L, s);
+    case 4: return launch_g<4>(a, list, min_L, max_L, s);
+    case 5: return launch_g<5>(a, list, min_L, max_L, s);
+    case 6: return launch_g<6>(a, list, min_L, max_L, s);
+    case 7: return launch_g<7>(a, list, min_L, max_L, s);
+    case 8: return launch_g<8>(a, list, min_L, max_L, s);
     default: return cudaErrorInvalidValue;
   }
-#undef GPOEO_SCORE_CASE
-  return cudaGetLastError();
 }
 
 }  // namespace gpoeo

@@ -31,13 +31,13 @@ __global__ void select_kernel(Plan p, Work w) {
   if (lo < p.Lmin) lo = p.Lmin;
   if (hi > p.Lmax) hi = p.Lmax;
   const int64_t cnt = hi - lo + 1;
-  const unsigned long long base = atomicAdd(&w.ctr[CTR_ITEMS_B], (unsigned long long)cnt);
+  // scores of this trace's local range live at local_err[base .. base + cnt)
+  const unsigned long long base = atomicAdd(&w.ctr[CTR_LOCAL_SLOTS], (unsigned long long)cnt);
   w.best_bin[t] = (int32_t)kb;
   w.local_lo[t] = (int32_t)lo;
   w.local_hi[t] = (int32_t)hi;
   w.local_base[t] = (int64_t)base;
-  for (int64_t i = 0; i < cnt; ++i)
-    w.items_b[base + i] = make_int4((int)t, (int)(lo + i), (int)(base + i), 0);
+  append_items(w.list_b, (int)t, (int)lo, (int)cnt, (int)base);
 }
 
 // One thread per trace: argmin (Err, L) over the local range -> result (+ detail).

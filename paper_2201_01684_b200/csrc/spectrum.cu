@@ -382,9 +382,7 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
       if (status == GPOEO_TRACE_OK && nc == 0) status = GPOEO_TRACE_APERIODIC;
       w.status[t] = status;
       if (status == GPOEO_TRACE_OK) {
-        const unsigned long long base = atomicAdd(&w.ctr[CTR_ITEMS_A], (unsigned long long)nc);
-        for (int c2 = 0; c2 < nc; ++c2)
-          w.items_a[base + c2] = make_int4((int)t, w.cand_L[t * p.K + c2], (int)(t * p.K + c2), 0);
+        for (int c2 = 0; c2 < nc; ++c2) append_item(w.list_a, (int)t, w.cand_L[t * p.K + c2], (int)(t * p.K + c2));
       }
     }
   }
