@@ -260,7 +260,7 @@ def run_gpu(args) -> None:
         "phase_ms": {n: float(v) for n, v in zip(g.PHASES, phase_ms)},
         "work_counters": counters,
         "clocks": clocks,
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": 8 * args.steps,  # composite, spectrum, 2x(team + bucket scorer), select, final
     }
 
     # e2e: same metric through the public host entry point (pinned host buffers, H2D+D2H inside)

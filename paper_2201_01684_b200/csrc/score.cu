@@ -357,7 +357,7 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 // margins (Z27). Cost per pass: O(K + straddled samples) instead of O(L).
 constexpr int kBuckets = 64;
 constexpr int kBucketMaxL = 8192;
-constexpr int kBucketWarps = 4;  // bucket-kernel CTA: 4 warps, one pair each
+constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order, no CTA barrier waits
 
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
   return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) + (size_t)kBuckets * 8 * 2 +
@@ -444,21 +444,23 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   constexpr int KPL = kBuckets / 32;  // buckets per lane
   const unsigned lt_mask = (1u << lane) - 1u;
   // ---- range of W_i ----------------------------------------------------------------
-  double mn = INFINITY, mx = -INFINITY;
+  float mnf = INFINITY, mxf = -INFINITY;
 #pragma unroll 4
   for (int s = lane; s < L; s += 32) {
-    const double v = (double)__ldg(A + s);
-    mn = fmin(mn, v);
-    mx = fmax(mx, v);
+    const float v = __ldg(A + s);
+    mnf = fminf(mnf, v);
+    mxf = fmaxf(mxf, v);
   }
 #pragma unroll 1
   for (int off = 16; off; off >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(FULL, mn, off));
-    mx = fmax(mx, __shfl_xor_sync(FULL, mx, off));
+    mnf = fminf(mnf, __shfl_xor_sync(FULL, mnf, off));
+    mxf = fmaxf(mxf, __shfl_xor_sync(FULL, mxf, off));
   }
+  const double mn = (double)mnf, mx = (double)mxf;  // exact
   const double R = mx - mn;
   if (!(R > 0.0) || G == 1) return 0.0;
-  const double bscale = (double)kBuckets / R;
+  // bucket of a value: any deterministic monotone map works (both sort loops use it)
+  const float bscale = (float)kBuckets / (mxf - mnf);
   // ---- stable counting sort of sample indices by value bucket ------------------------
   for (int b = lane; b <= kBuckets; b += 32) bv.off[b] = 0;
   __syncwarp();
@@ -467,8 +469,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     const int s = s0 + lane;
     int b = kBuckets;
     if (s < L) {
-      b = (int)(((double)__ldg(A + s) - mn) * bscale);
-      b = b > kBuckets - 1 ? kBuckets - 1 : b;
+      b = (int)((__ldg(A + s) - mnf) * bscale);
+      b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
     }
     const unsigned peers = __match_any_sync(FULL, b);
     if (b < kBuckets && (peers & lt_mask) == 0) bv.off[b + 1] += (uint16_t)__popc(peers);
@@ -505,8 +507,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     const int s = s0 + lane;
     int b = kBuckets;
     if (s < L) {
-      b = (int)(((double)__ldg(A + s) - mn) * bscale);
-      b = b > kBuckets - 1 ? kBuckets - 1 : b;
+      b = (int)((__ldg(A + s) - mnf) * bscale);
+      b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
     }
     const unsigned peers = __match_any_sync(FULL, b);
     int base = 0;
@@ -577,6 +579,35 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         }
         if (it == 1) { cj = ck = 0.0; hj = hk = 1.0; }  // first pass: argmin (y - mu)^2
         score_crossings(muj, cj, hj, muk, ck, hk, mn, r0, r1);
+        // keep only crossings on the upper envelope: if a third component beats both
+        // clearly at the crossing, the winner there is that component and the pair's
+        // crossing cannot change any label (the margin absorbs root rounding).
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const double r = rr ? r1 : r0;
+          if (r != r) continue;  // NaN: no root
+          double sj;
+          if (it == 1) {
+            const double d = r - muj;
+            sj = -d * d;
+          } else {
+            const double d = r - muj;
+            sj = cj - hj * d * d;
+          }
+          bool dominated = false;
+#pragma unroll
+          for (int m = 0; m < G; ++m) {
+            if (m == pj || m == pk) continue;
+            double sm;
+            const double d = r - cem.mu[m];
+            if (it == 1) sm = -d * d;
+            else sm = cem.c[m] == -INFINITY ? -INFINITY : cem.c[m] - cem.h[m] * d * d;
+            dominated |= sm > sj + 1e-6 * (fabs(sj) + fabs(sm) + 1.0);
+          }
+          if (dominated) {
+            if (rr) r1 = NAN; else r0 = NAN;
+          }
+        }
       }
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -921,12 +952,12 @@ static int device_sms() {
 }
 
 template <typename K>
-static int grid_of(K kern, int threads, size_t smem) {
+static int grid_of(K kern, int threads, size_t smem, int cap) {
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (occ < 1) occ = 1;
   const int g = device_sms() * occ;
-  return g < kMaxScoreCtas ? g : kMaxScoreCtas;
+  return g < cap ? g : cap;
 }
 
 template <int G>
@@ -938,7 +969,7 @@ static cudaError_t launch_g(const ScoreArgs& base, const ItemList& list, int32_t
     a.cursor = list.cur_small;
     a.reverse = 0;
     auto kern = score_team_kernel<G>;
-    score_team_kernel<G><<<grid_of(kern, kScoreThreads, 0), kScoreThreads, 0, s>>>(a);
+    score_team_kernel<G><<<grid_of(kern, kScoreThreads, 0, kMaxScoreCtas), kScoreThreads, 0, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -953,7 +984,9 @@ static cudaError_t launch_g(const ScoreArgs& base, const ItemList& list, int32_t
     auto kern = score_bucket_kernel<G>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    score_bucket_kernel<G><<<grid_of(kern, kBucketWarps * 32, smem), kBucketWarps * 32, smem, s>>>(a);
+    // label-scratch slots exist for kMaxScoreCtas * kWarps warps (gpoeo_api.cu layout)
+    score_bucket_kernel<G><<<grid_of(kern, kBucketWarps * 32, smem, kMaxScoreCtas * kWarps / kBucketWarps),
+                             kBucketWarps * 32, smem, s>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
