@@ -173,9 +173,13 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   Work w = carve(pl, L, ws);
   CK(mark(0));
   CK(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
-  if (pl.batch > 0) CK(launch_composite(traces, pl, w.y, w.status, s));
+  const bool fused = pl.N == 65536;  // configs 3/4: one kernel reads x once (spectrum.cu)
+  if (pl.batch > 0 && !fused) CK(launch_composite(traces, pl, w.y, w.status, s));
   CK(mark(1));
-  if (pl.batch > 0) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
+  if (pl.batch > 0) {
+    if (fused) CK(launch_spectral_fused(pl, traces, w, w.y, nullptr, true, s));
+    else CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
+  }
   CK(mark(2));
   if (pl.batch > 0)
     CK(launch_score(pl, w.y, w.list_a, w.cand_err, w.lab_scratch, L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmin,
@@ -346,6 +350,10 @@ int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params*
   Work w = carve(pl, L, workspace);
   if (batch == 0) return GPOEO_OK;
   float* y = signal ? signal : w.y;
+  if (pl.N == 65536) {
+    CK(launch_spectral_fused(pl, traces, w, y, spectra, false, s));
+    return GPOEO_OK;
+  }
   CK(launch_composite(traces, pl, y, w.status, s));
   if (spectra) CK(launch_spectrum(pl, y, w.status, w, spectra, false, s));
   return GPOEO_OK;

@@ -156,6 +156,133 @@ struct PView {
   }
 };
 
+// Rows a3: in-band peaks -> top-K (P desc, k asc) -> c_peak threshold -> L = floor(N/k) ->
+// dedupe (Alg.1 l.3-5; Z5, Z7-Z9); appends one Alg. 2 query per candidate and
+// writes the trace status. Called by the whole CTA (T threads) of cluster rank 0.
+template <int C, int T>
+__device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = T / 32;
+  // pass 1: P_max over in-band peaks
+  float best = -1.f;
+  for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
+    const float pk = Pv(k);
+    if (pk > Pv(k - 1) && pk >= Pv(k + 1)) best = fmaxf(best, pk);
+  }
+  for (int off = 16; off; off >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
+  if (lane == 0) ps.redP[warp] = best;
+  if (threadIdx.x == 0) { ps.count = 0; ps.overflow = 0; }
+  __syncthreads();
+  float pmax = -1.f;
+  for (int i = 0; i < NW; ++i) pmax = fmaxf(pmax, ps.redP[i]);
+  const double thr = (double)p.c_peak * (double)p.c_peak * (double)pmax;
+  int nc = 0;
+  if (pmax >= 0.f) {
+    // pass 2: peaks above the threshold
+    for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
+      const float pk = Pv(k);
+      if (pk > Pv(k - 1) && pk >= Pv(k + 1) && (double)pk > thr) {
+        const int slot = atomicAdd(&ps.count, 1);
+        if (slot < kPeakCap) {
+          ps.pk_P[slot] = pk;
+          ps.pk_k[slot] = (int32_t)k;
+        }
+      }
+    }
+    __syncthreads();
+    const int cnt = ps.count;
+    if (cnt <= kPeakCap) {
+      // rank sort by (P desc, k asc): rank = number of entries ahead
+      for (int e = threadIdx.x; e < cnt; e += T) {
+        const float pe = ps.pk_P[e];
+        const int32_t ke = ps.pk_k[e];
+        int rank = 0;
+        for (int f = 0; f < cnt; ++f) {
+          const float pf = ps.pk_P[f];
+          rank += (pf > pe) || (pf == pe && ps.pk_k[f] < ke);
+        }
+        ps.sorted[rank] = e;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int lim = cnt < p.K ? cnt : p.K;
+        for (int r = 0; r < lim; ++r) {
+          const int e = ps.sorted[r];
+          const int32_t k = ps.pk_k[e];
+          const int32_t L = p.N / k;
+          bool dup = false;
+          for (int c2 = 0; c2 < nc; ++c2) dup |= (w.cand_L[t * p.K + c2] == L);
+          if (dup) continue;
+          w.cand_k[t * p.K + nc] = k;
+          w.cand_L[t * p.K + nc] = L;
+          w.cand_P[t * p.K + nc] = ps.pk_P[e];
+          ++nc;
+        }
+        ps.count = nc;
+      }
+    } else {
+      // rare: more than kPeakCap peaks pass. K rounds of block arg-max in (P desc, k asc);
+      // every thread ends each round with the same (bp, bk).
+      float prevP = INFINITY;
+      int32_t prevk = -1;
+      for (int r = 0; r < p.K; ++r) {
+        float bp = -1.f;
+        int32_t bk = 0x7fffffff;
+        for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
+          const float pk = Pv(k);
+          if (!(pk > Pv(k - 1) && pk >= Pv(k + 1) && (double)pk > thr)) continue;
+          const bool after = (pk < prevP) || (pk == prevP && (int32_t)k > prevk);
+          if (!after) continue;
+          if (pk > bp || (pk == bp && (int32_t)k < bk)) { bp = pk; bk = (int32_t)k; }
+        }
+        for (int off = 16; off; off >>= 1) {
+          const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+          const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+          if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+        }
+        __syncthreads();
+        if (lane == 0) { ps.redP[warp] = bp; ps.redk[warp] = bk; }
+        __syncthreads();
+        bp = -1.f;
+        bk = 0x7fffffff;
+        for (int i = 0; i < NW; ++i) {
+          const float op = ps.redP[i];
+          const int32_t ok = ps.redk[i];
+          if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+        }
+        if (bp < 0.f) break;
+        if (threadIdx.x == 0) {
+          const int32_t L = p.N / bk;
+          bool dup = false;
+          for (int c2 = 0; c2 < nc; ++c2) dup |= (w.cand_L[t * p.K + c2] == L);
+          if (!dup) {
+            w.cand_k[t * p.K + nc] = bk;
+            w.cand_L[t * p.K + nc] = L;
+            w.cand_P[t * p.K + nc] = bp;
+            ++nc;
+          }
+        }
+        prevP = bp;
+        prevk = bk;
+      }
+      if (threadIdx.x == 0) ps.count = nc;
+    }
+    __syncthreads();
+    nc = ps.count;
+  }
+  if (threadIdx.x == 0) {
+    w.n_cand[t] = nc;
+    int32_t status = st;
+    if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;  // empty band (Z21)
+    if (status == GPOEO_TRACE_OK && nc == 0) status = GPOEO_TRACE_APERIODIC;
+    w.status[t] = status;
+    if (status == GPOEO_TRACE_OK) {
+      for (int c2 = 0; c2 < nc; ++c2) append_item(w.list_a, (int)t, w.cand_L[t * p.K + c2], (int)(t * p.K + c2));
+    }
+  }
+
+}
+
 template <int LOGN2, int C>
 __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, const float* __restrict__ y,
                                                                     const int32_t* __restrict__ status_in, Work w,
@@ -265,126 +392,7 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
     } else {
       Pv.base[0] = P;
     }
-    const int32_t st = status_in[t];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = T / 32;
-    // pass 1: P_max over in-band peaks
-    float best = -1.f;
-    for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
-      const float pk = Pv(k);
-      if (pk > Pv(k - 1) && pk >= Pv(k + 1)) best = fmaxf(best, pk);
-    }
-    for (int off = 16; off; off >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-    if (lane == 0) ps.redP[warp] = best;
-    if (threadIdx.x == 0) { ps.count = 0; ps.overflow = 0; }
-    __syncthreads();
-    float pmax = -1.f;
-    for (int i = 0; i < NW; ++i) pmax = fmaxf(pmax, ps.redP[i]);
-    const double thr = (double)p.c_peak * (double)p.c_peak * (double)pmax;
-    int nc = 0;
-    if (pmax >= 0.f) {
-      // pass 2: peaks above the threshold
-      for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
-        const float pk = Pv(k);
-        if (pk > Pv(k - 1) && pk >= Pv(k + 1) && (double)pk > thr) {
-          const int slot = atomicAdd(&ps.count, 1);
-          if (slot < kPeakCap) {
-            ps.pk_P[slot] = pk;
-            ps.pk_k[slot] = (int32_t)k;
-          }
-        }
-      }
-      __syncthreads();
-      const int cnt = ps.count;
-      if (cnt <= kPeakCap) {
-        // rank sort by (P desc, k asc): rank = number of entries ahead
-        for (int e = threadIdx.x; e < cnt; e += T) {
-          const float pe = ps.pk_P[e];
-          const int32_t ke = ps.pk_k[e];
-          int rank = 0;
-          for (int f = 0; f < cnt; ++f) {
-            const float pf = ps.pk_P[f];
-            rank += (pf > pe) || (pf == pe && ps.pk_k[f] < ke);
-          }
-          ps.sorted[rank] = e;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          const int lim = cnt < p.K ? cnt : p.K;
-          for (int r = 0; r < lim; ++r) {
-            const int e = ps.sorted[r];
-            const int32_t k = ps.pk_k[e];
-            const int32_t L = p.N / k;
-            bool dup = false;
-            for (int c2 = 0; c2 < nc; ++c2) dup |= (w.cand_L[t * p.K + c2] == L);
-            if (dup) continue;
-            w.cand_k[t * p.K + nc] = k;
-            w.cand_L[t * p.K + nc] = L;
-            w.cand_P[t * p.K + nc] = ps.pk_P[e];
-            ++nc;
-          }
-          ps.count = nc;
-        }
-      } else {
-        // rare: more than kPeakCap peaks pass. K rounds of block arg-max in (P desc, k asc);
-        // every thread ends each round with the same (bp, bk).
-        float prevP = INFINITY;
-        int32_t prevk = -1;
-        for (int r = 0; r < p.K; ++r) {
-          float bp = -1.f;
-          int32_t bk = 0x7fffffff;
-          for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
-            const float pk = Pv(k);
-            if (!(pk > Pv(k - 1) && pk >= Pv(k + 1) && (double)pk > thr)) continue;
-            const bool after = (pk < prevP) || (pk == prevP && (int32_t)k > prevk);
-            if (!after) continue;
-            if (pk > bp || (pk == bp && (int32_t)k < bk)) { bp = pk; bk = (int32_t)k; }
-          }
-          for (int off = 16; off; off >>= 1) {
-            const float op = __shfl_xor_sync(0xffffffffu, bp, off);
-            const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
-            if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
-          }
-          __syncthreads();
-          if (lane == 0) { ps.redP[warp] = bp; ps.redk[warp] = bk; }
-          __syncthreads();
-          bp = -1.f;
-          bk = 0x7fffffff;
-          for (int i = 0; i < NW; ++i) {
-            const float op = ps.redP[i];
-            const int32_t ok = ps.redk[i];
-            if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
-          }
-          if (bp < 0.f) break;
-          if (threadIdx.x == 0) {
-            const int32_t L = p.N / bk;
-            bool dup = false;
-            for (int c2 = 0; c2 < nc; ++c2) dup |= (w.cand_L[t * p.K + c2] == L);
-            if (!dup) {
-              w.cand_k[t * p.K + nc] = bk;
-              w.cand_L[t * p.K + nc] = L;
-              w.cand_P[t * p.K + nc] = bp;
-              ++nc;
-            }
-          }
-          prevP = bp;
-          prevk = bk;
-        }
-        if (threadIdx.x == 0) ps.count = nc;
-      }
-      __syncthreads();
-      nc = ps.count;
-    }
-    if (threadIdx.x == 0) {
-      w.n_cand[t] = nc;
-      int32_t status = st;
-      if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;  // empty band (Z21)
-      if (status == GPOEO_TRACE_OK && nc == 0) status = GPOEO_TRACE_APERIODIC;
-      w.status[t] = status;
-      if (status == GPOEO_TRACE_OK) {
-        for (int c2 = 0; c2 < nc; ++c2) append_item(w.list_a, (int)t, w.cand_L[t * p.K + c2], (int)(t * p.K + c2));
-      }
-    }
+    find_candidates<C, T>(p, Pv, t, status_in[t], w, ps);
   }
   if constexpr (C > 1) cg::this_cluster().sync();  // keep our P alive while rank 0 reads it
 }
@@ -411,6 +419,306 @@ static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* s
   e = cudaLaunchKernelEx(&cfg, kern, p, y, status_in, w, spectra, find_peaks);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// ===================================================================================
+// Fused rows a1 + a2 + a3 for N = 65536 (BASELINE configs 3 and 4): the composite, the
+// FFT power spectrum and the peak picking in ONE persistent kernel per 2-CTA cluster, so
+// the trace x[F][N] is read from HBM once (the stats pass and the signal pass touch the
+// same two quarter-blocks per CTA; the second read is an L2 hit) and y is written once
+// (for the Alg. 2 scorer). Same arithmetic as composite_kernel + spectrum_kernel<14, 2>:
+//   stats: fp64 sums, shifted by x_c[0]; CTA partials added in rank order;
+//   y = fp32(sum_c a_c (x_c - mu_c)) with _rn intrinsics;
+//   DIF split a_0[j] = z[j] + z[j + n2], a_1[j] = (z[j] - z[j + n2]) W_n^j built while y
+//   is formed (CTA q owns j in [q n2/2, (q+1) n2/2) and stores the other half into its
+//   partner's shared memory through DSMEM);
+//   n2 = 16384-point FFT: three in-place Stockham passes (radix 32, 32, 16) with the
+//   butterflies in registers, twiddles from a quarter-wave table in shared memory, one
+//   pad slot per 32 entries (conflict-free strided writes).
+namespace fz {
+constexpr int kN = 65536, kn = 32768, kn2 = 16384, kT = 512;
+constexpr int kBuf = kn2 + kn2 / 32;  // padded float2 entries
+constexpr int kTw = kn2 / 4;          // quarter-wave table W_16384^m, m < 4096
+__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
+
+__constant__ float2 kW32[22] = {
+    {1.000000000e+00f, -0.000000000e+00f}, {9.807852804e-01f, -1.950903220e-01f}, {9.238795325e-01f, -3.826834324e-01f},
+    {8.314696123e-01f, -5.555702330e-01f}, {7.071067812e-01f, -7.071067812e-01f}, {5.555702330e-01f, -8.314696123e-01f},
+    {3.826834324e-01f, -9.238795325e-01f}, {1.950903220e-01f, -9.807852804e-01f}, {0.0f, -1.000000000e+00f},
+    {-1.950903220e-01f, -9.807852804e-01f}, {-3.826834324e-01f, -9.238795325e-01f}, {-5.555702330e-01f, -8.314696123e-01f},
+    {-7.071067812e-01f, -7.071067812e-01f}, {-8.314696123e-01f, -5.555702330e-01f}, {-9.238795325e-01f, -3.826834324e-01f},
+    {-9.807852804e-01f, -1.950903220e-01f}, {-1.000000000e+00f, 0.0f}, {-9.807852804e-01f, 1.950903220e-01f},
+    {-9.238795325e-01f, 3.826834324e-01f}, {-8.314696123e-01f, 5.555702330e-01f}, {-7.071067812e-01f, 7.071067812e-01f},
+    {-5.555702330e-01f, 8.314696123e-01f}};
+
+// W_16384^m from the quarter table: W^m = (-i)^(m >> 12) * tw[m & 4095]
+__device__ __forceinline__ float2 twiddle(const float2* tw, int m) {
+  const float2 b = tw[m & (kTw - 1)];
+  switch ((m >> 12) & 3) {
+    case 0: return b;
+    case 1: return make_float2(b.y, -b.x);
+    case 2: return make_float2(-b.x, -b.y);
+    default: return make_float2(-b.y, b.x);
+  }
+}
+
+// In-place 32-point DFT: n = 8 n1 + n2, k = k1 + 4 k2: DFT4 over n1 (elements n2 + 8 n1),
+// twiddle W32^(n2 k1), DFT8 over n2 (elements 8 k1 .. 8 k1 + 7). Output X[k1 + 4 k2] is left
+// at v[k2 + 8 k1] (see out32).
+__device__ __forceinline__ void dft32(float2* v) {
+#pragma unroll
+  for (int n2 = 0; n2 < 8; ++n2) {
+    float2 a[4] = {v[n2], v[8 + n2], v[16 + n2], v[24 + n2]};
+    dft<4>(a);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) v[n2 + 8 * k1] = (n2 * k1 == 0) ? a[k1] : cmul(a[k1], kW32[n2 * k1]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft<8>(v + 8 * k1);
+}
+__device__ __forceinline__ constexpr int out32(int r) { return (r >> 2) + 8 * (r & 3); }
+
+// In-place 16-point DFT: n = 4 n1 + n2, k = k1 + 4 k2; X[k1 + 4 k2] left at v[k2 + 4 k1].
+__device__ __forceinline__ void dft16(float2* v) {
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    float2 a[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+    dft<4>(a);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) v[n2 + 4 * k1] = (n2 * k1 == 0) ? a[k1] : cmul(a[k1], kW32[2 * n2 * k1]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft<4>(v + 4 * k1);
+}
+__device__ __forceinline__ constexpr int out16(int r) { return (r >> 2) + 4 * (r & 3); }
+
+template <int R>
+__device__ __forceinline__ void pass(float2* buf, const float2* tw, int Ns) {
+  constexpr int NB = kn2 / R;
+  constexpr int PER = NB / kT;
+  float2 v[PER][R];
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int j = threadIdx.x + b * kT;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = buf[pad(j + r * NB)];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int j = threadIdx.x + b * kT;
+    const int k = j & (Ns - 1);
+    if (Ns > 1) {
+      const int step = k * (kn2 / (Ns * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], twiddle(tw, step * r));
+    }
+    if constexpr (R == 32) dft32(v[b]);
+    else dft16(v[b]);
+    const int dst = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pad(dst + r * Ns)] = v[b][R == 32 ? out32(r) : out16(r)];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double block_sum512(double v, double* red) {
+  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < kT / 32; ++i) s += red[i];
+  return s;
+}
+
+struct FusedShared {
+  PeakShared ps;
+  double red[kT / 32];
+  double mu[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
+  double stat[2][GPOEO_MAX_FEATURES][2];  // [rank][channel][sum, shifted sum of squares]
+};
+constexpr size_t kDynSmem = (size_t)kBuf * sizeof(float2) + (size_t)kTw * sizeof(float2);
+}  // namespace fz
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
+    fused_spectrum_65536(Plan p, const float* __restrict__ x, Work w, float* __restrict__ y_out,
+                         float* __restrict__ spectra, int find_peaks, int nclusters) {
+  using namespace fz;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* buf = reinterpret_cast<float2*>(smem_raw);
+  float2* tw = buf + kBuf;
+  __shared__ FusedShared fs;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const int cid = blockIdx.x / 2;
+  float2* pbuf = cluster.map_shared_rank(buf, q ^ 1);
+  for (int m = threadIdx.x; m < kTw; m += kT) {
+    float s, c;
+    sincospif(-2.0f * (float)m / (float)kn2, &s, &c);
+    tw[m] = make_float2(c, s);
+  }
+  const float2 w32768 = make_float2(9.999999816164e-01f, -1.917475973107e-04f);
+  const int F = p.F;
+  for (int64_t t = cid; t < p.batch; t += nclusters) {
+    const float* xt = x + t * p.stride;
+    // ---- a1 stats over my quarter blocks {q, 2 + q} ----------------------------------
+    double* mu = fs.mu;
+    double* a = fs.a;
+    for (int c = 0; c < F; ++c) {
+      const float* xc = xt + (int64_t)c * kN;
+      const double x0 = (double)__ldg(xc);
+      double s = 0.0, qq = 0.0;
+      const float4* x4 = reinterpret_cast<const float4*>(xc);
+      for (int i = threadIdx.x; i < kn2 / 2; i += kT) {  // 2 blocks x 4096 float4
+        const int blk = (i < kn2 / 4) ? q : 2 + q;
+        const float4 v = __ldg(x4 + blk * (kn2 / 4) + (i & (kn2 / 4 - 1)));
+        const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
+        s += v0; s += v1; s += v2; s += v3;
+        const double d0 = v0 - x0, d1 = v1 - x0, d2 = v2 - x0, d3 = v3 - x0;
+        qq = __fma_rn(d0, d0, qq); qq = __fma_rn(d1, d1, qq); qq = __fma_rn(d2, d2, qq); qq = __fma_rn(d3, d3, qq);
+      }
+      s = block_sum512(s, fs.red);
+      qq = block_sum512(qq, fs.red);
+      if (threadIdx.x == 0) {
+        fs.stat[q][c][0] = s;
+        fs.stat[q][c][1] = qq;
+        FusedShared* pfs = cluster.map_shared_rank(&fs, q ^ 1);
+        pfs->stat[q][c][0] = s;
+        pfs->stat[q][c][1] = qq;
+      }
+      (void)x0;
+    }
+    cluster.sync();
+    bool all_const = true;
+    for (int c = 0; c < F; ++c) {
+      const double x0 = (double)__ldg(xt + (int64_t)c * kN);
+      const double s = fs.stat[0][c][0] + fs.stat[1][c][0];
+      const double qq = fs.stat[0][c][1] + fs.stat[1][c][1];
+      const double muc = s / (double)kN;
+      const double m = muc - x0;
+      double var = qq / (double)kN - m * m;
+      if (!(var > 0.0)) var = 0.0;
+      const double sigma = sqrt(var);
+      if (threadIdx.x == 0) {
+        mu[c] = muc;
+        a[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
+      }
+      if (sigma > 0.0) all_const = false;
+    }
+    __syncthreads();
+    // ---- a1 signal + DIF split into the two CTAs' buffers ------------------------------
+    float* yt = y_out + t * (int64_t)kN;
+    for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
+      const int j = q * (kn2 / 2) + jj;
+      double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+      for (int c = 0; c < F; ++c) {
+        if (a[c] == 0.0) continue;
+        const float* xc = xt + (int64_t)c * kN;
+        const float2 xa = __ldg(reinterpret_cast<const float2*>(xc + 2 * j));
+        const float2 xb = __ldg(reinterpret_cast<const float2*>(xc + 2 * j + kn));
+        ya0 = __dadd_rn(ya0, __dmul_rn(a[c], __dsub_rn((double)xa.x, mu[c])));
+        ya1 = __dadd_rn(ya1, __dmul_rn(a[c], __dsub_rn((double)xa.y, mu[c])));
+        yb0 = __dadd_rn(yb0, __dmul_rn(a[c], __dsub_rn((double)xb.x, mu[c])));
+        yb1 = __dadd_rn(yb1, __dmul_rn(a[c], __dsub_rn((double)xb.y, mu[c])));
+      }
+      const float2 za = make_float2(__double2float_rn(ya0), __double2float_rn(ya1));
+      const float2 zb = make_float2(__double2float_rn(yb0), __double2float_rn(yb1));
+      reinterpret_cast<float2*>(yt)[j] = za;
+      reinterpret_cast<float2*>(yt + kn)[j] = zb;
+      const float2 a0 = cadd(za, zb);
+      float2 wj = twiddle(tw, j >> 1);  // W_32768^j = W_16384^(j/2) (x W_32768 if j odd)
+      if (j & 1) wj = cmul(wj, w32768);
+      const float2 a1 = cmul(csub(za, zb), wj);
+      buf[pad(j)] = q == 0 ? a0 : a1;
+      pbuf[pad(j)] = q == 0 ? a1 : a0;
+    }
+    cluster.sync();
+    // ---- a2 FFT (16384 points per CTA) -----------------------------------------------
+    pass<32>(buf, tw, 1);
+    pass<32>(buf, tw, 32);
+    pass<16>(buf, tw, 1024);
+    // ---- R2C post: P[2 k2 + q] (C = 2: partner bins sit in the same CTA) ---------------
+    constexpr int PER = kn2 / kT;
+    float pv[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int k2 = threadIdx.x + i * kT;
+      const int k = 2 * k2 + q;
+      const float2 Zk = buf[pad(k2)];
+      const float2 Zp = (q == 0) ? buf[pad((kn2 - k2) & (kn2 - 1))] : buf[pad(kn2 - 1 - k2)];
+      const float2 E = make_float2(0.5f * (Zk.x + Zp.x), 0.5f * (Zk.y - Zp.y));
+      const float2 O = make_float2(0.5f * (Zk.y + Zp.y), -0.5f * (Zk.x - Zp.x));
+      float s, c;
+      sincospif(-2.0f * (float)k / (float)kN, &s, &c);
+      const float2 X = cadd(E, cmul(make_float2(c, s), O));
+      pv[i] = X.x * X.x + X.y * X.y;
+    }
+    float pnyq = 0.f;
+    if (q == 0 && threadIdx.x == 0) {
+      const float2 Z0 = buf[0];
+      const float xr = Z0.x - Z0.y;
+      pnyq = xr * xr;
+    }
+    __syncthreads();
+    float* P = reinterpret_cast<float*>(buf);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int k2 = threadIdx.x + i * kT;
+      P[k2] = pv[i];
+      if (spectra) spectra[t * (int64_t)(kn + 1) + 2 * k2 + q] = pv[i];
+    }
+    if (q == 0 && threadIdx.x == 0) {
+      P[kn2] = pnyq;
+      if (spectra) spectra[t * (int64_t)(kn + 1) + kn] = pnyq;
+    }
+    cluster.sync();
+    // ---- a3 peaks -> candidates (rank 0) ------------------------------------------------
+    if (q == 0) {
+      const int32_t st = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
+      if (find_peaks) {
+        PView<2> Pv;
+        Pv.n = kn;
+        Pv.base[0] = P;
+        Pv.base[1] = cluster.map_shared_rank(P, 1);
+        find_candidates<2, kT>(p, Pv, t, st, w, fs.ps);
+      } else if (threadIdx.x == 0) {
+        w.status[t] = st;
+      }
+    }
+    cluster.sync();  // partner P read; buffers free for the next trace
+  }
+}
+
+static cudaError_t launch_fused_65536(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
+                                      bool find_peaks, cudaStream_t s) {
+  auto kern = fused_spectrum_65536;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::kDynSmem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(fz::kT);
+  cfg.dynamicSmemBytes = fz::kDynSmem;
+  cfg.stream = s;
+  cfg.gridDim = dim3(2);
+  int nclust = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclust, (void*)kern, &cfg) != cudaSuccess || nclust < 1) {
+    cudaGetLastError();
+    nclust = 64;
+  }
+  if ((int64_t)nclust > p.batch) nclust = (int)p.batch;
+  cfg.gridDim = dim3(2 * nclust);
+  e = cudaLaunchKernelEx(&cfg, kern, p, x, w, y_out, spectra, find_peaks ? 1 : 0, nclust);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
+                                  bool find_peaks, cudaStream_t s) {
+  if (p.batch == 0) return cudaSuccess;
+  if (p.N != fz::kN) return cudaErrorInvalidValue;
+  return launch_fused_65536(p, x, w, y_out, spectra, find_peaks, s);
 }
 
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
