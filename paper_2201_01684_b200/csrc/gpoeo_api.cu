@@ -173,7 +173,7 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   Work w = carve(pl, L, ws);
   CK(mark(0));
   CK(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
-  const bool fused = pl.N == 65536;  // configs 3/4: one kernel reads x once (spectrum.cu)
+  const bool fused = pl.N == 65536 && pl.F <= 3;  // configs 3/4: one kernel reads x once (spectrum.cu)
   if (pl.batch > 0 && !fused) CK(launch_composite(traces, pl, w.y, w.status, s));
   CK(mark(1));
   if (pl.batch > 0) {
@@ -350,7 +350,7 @@ int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params*
   Work w = carve(pl, L, workspace);
   if (batch == 0) return GPOEO_OK;
   float* y = signal ? signal : w.y;
-  if (pl.N == 65536) {
+  if (pl.N == 65536 && pl.F <= 3) {
     CK(launch_spectral_fused(pl, traces, w, y, spectra, false, s));
     return GPOEO_OK;
   }

@@ -882,12 +882,16 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
       if (has) acc += e;
     }
     if (lt != 0) acc = 0.0;
-    // per-team partials -> Err(L), in team order
-    s_team[tid] = acc;
+    // per-team partials -> Err(L): fixed-shape tree (xor butterfly per warp, then warps in
+    // order), so the rounding is identical on every run
+#pragma unroll
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
+    if (lane == 0) s_team[warp] = acc;
     __syncthreads();
     if (tid == 0) {
       double sum = 0.0;
-      for (int tm = 0; tm < kScoreThreads; tm += tau) sum += s_team[tm];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) sum += s_team[w];
       a.err_out[q.z] = sum / (double)npairs;
     }
     __syncthreads();

@@ -537,12 +537,12 @@ __device__ __forceinline__ double block_sum512(double v, double* red) {
 struct FusedShared {
   PeakShared ps;
   double red[kT / 32];
-  double mu[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
   double stat[2][GPOEO_MAX_FEATURES][2];  // [rank][channel][sum, shifted sum of squares]
 };
 constexpr size_t kDynSmem = (size_t)kBuf * sizeof(float2) + (size_t)kTw * sizeof(float2);
 }  // namespace fz
 
+template <int F>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     fused_spectrum_65536(Plan p, const float* __restrict__ x, Work w, float* __restrict__ y_out,
                          float* __restrict__ spectra, int find_peaks, int nclusters) {
@@ -561,12 +561,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     tw[m] = make_float2(c, s);
   }
   const float2 w32768 = make_float2(9.999999816164e-01f, -1.917475973107e-04f);
-  const int F = p.F;
   for (int64_t t = cid; t < p.batch; t += nclusters) {
     const float* xt = x + t * p.stride;
     // ---- a1 stats over my quarter blocks {q, 2 + q} ----------------------------------
-    double* mu = fs.mu;
-    double* a = fs.a;
+    double mu[F], a[F];
+#pragma unroll
     for (int c = 0; c < F; ++c) {
       const float* xc = xt + (int64_t)c * kN;
       const double x0 = (double)__ldg(xc);
@@ -593,27 +592,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     }
     cluster.sync();
     bool all_const = true;
+#pragma unroll
     for (int c = 0; c < F; ++c) {
       const double x0 = (double)__ldg(xt + (int64_t)c * kN);
       const double s = fs.stat[0][c][0] + fs.stat[1][c][0];
       const double qq = fs.stat[0][c][1] + fs.stat[1][c][1];
-      const double muc = s / (double)kN;
-      const double m = muc - x0;
+      mu[c] = s / (double)kN;
+      const double m = mu[c] - x0;
       double var = qq / (double)kN - m * m;
       if (!(var > 0.0)) var = 0.0;
       const double sigma = sqrt(var);
-      if (threadIdx.x == 0) {
-        mu[c] = muc;
-        a[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
-      }
+      a[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
       if (sigma > 0.0) all_const = false;
     }
-    __syncthreads();
     // ---- a1 signal + DIF split into the two CTAs' buffers ------------------------------
     float* yt = y_out + t * (int64_t)kN;
     for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
       const int j = q * (kn2 / 2) + jj;
       double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+#pragma unroll
       for (int c = 0; c < F; ++c) {
         if (a[c] == 0.0) continue;
         const float* xc = xt + (int64_t)c * kN;
@@ -692,9 +689,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
   }
 }
 
+template <int F>
 static cudaError_t launch_fused_65536(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
                                       bool find_peaks, cudaStream_t s) {
-  auto kern = fused_spectrum_65536;
+  auto kern = fused_spectrum_65536<F>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::kDynSmem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -718,7 +716,12 @@ cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* 
                                   bool find_peaks, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
   if (p.N != fz::kN) return cudaErrorInvalidValue;
-  return launch_fused_65536(p, x, w, y_out, spectra, find_peaks, s);
+  switch (p.F) {
+    case 1: return launch_fused_65536<1>(p, x, w, y_out, spectra, find_peaks, s);
+    case 2: return launch_fused_65536<2>(p, x, w, y_out, spectra, find_peaks, s);
+    case 3: return launch_fused_65536<3>(p, x, w, y_out, spectra, find_peaks, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
