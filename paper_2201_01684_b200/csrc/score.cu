@@ -355,7 +355,13 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 // label changed" is exact. The final W_i / W_{i+1} pass walks the slots in one order for
 // both windows (Z28). Decisions equal the per-sample evaluation except at sub-rounding
 // margins (Z27). Cost per pass: O(K + straddled samples) instead of O(L).
-constexpr int kBuckets = 64;
+#ifndef GPOEO_BUCKETS
+#define GPOEO_BUCKETS 32
+#endif
+#ifndef GPOEO_BUCKET_MINB
+#define GPOEO_BUCKET_MINB 16  // resident one-warp CTAs per SM the register budget targets
+#endif
+constexpr int kBuckets = GPOEO_BUCKETS;
 constexpr int kBucketMaxL = 8192;
 constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order, no CTA barrier waits
 
@@ -464,17 +470,23 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // ---- stable counting sort of sample indices by value bucket ------------------------
   for (int b = lane; b <= kBuckets; b += 32) bv.off[b] = 0;
   __syncwarp();
+  auto bucket_of = [&](int s) -> int {
+    if (s >= L) return kBuckets;
+    const int b = (int)((__ldg(A + s) - mnf) * bscale);
+    return b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
+  };
 #pragma unroll 1
-  for (int s0 = 0; s0 < L; s0 += 32) {
-    const int s = s0 + lane;
-    int b = kBuckets;
-    if (s < L) {
-      b = (int)((__ldg(A + s) - mnf) * bscale);
-      b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
+  for (int s0 = 0; s0 < L; s0 += 128) {
+    int bb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bb[u] = bucket_of(s0 + 32 * u + lane);  // 4 loads in flight
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = bb[u];
+      const unsigned peers = __match_any_sync(FULL, b);
+      if (b < kBuckets && (peers & lt_mask) == 0) bv.off[b + 1] += (uint16_t)__popc(peers);
+      __syncwarp();
     }
-    const unsigned peers = __match_any_sync(FULL, b);
-    if (b < kBuckets && (peers & lt_mask) == 0) bv.off[b + 1] += (uint16_t)__popc(peers);
-    __syncwarp();
   }
   {
     // exclusive prefix over buckets: lane owns KPL consecutive counters
@@ -503,22 +515,23 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     __syncwarp();
   }
 #pragma unroll 1
-  for (int s0 = 0; s0 < L; s0 += 32) {
-    const int s = s0 + lane;
-    int b = kBuckets;
-    if (s < L) {
-      b = (int)((__ldg(A + s) - mnf) * bscale);
-      b = b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
+  for (int s0 = 0; s0 < L; s0 += 128) {
+    int bb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bb[u] = bucket_of(s0 + 32 * u + lane);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = bb[u];
+      const unsigned peers = __match_any_sync(FULL, b);
+      int base = 0;
+      if (b < kBuckets) {
+        base = bv.cur[b];
+        bv.pos[base + __popc(peers & lt_mask)] = (uint16_t)(s0 + 32 * u + lane);
+      }
+      __syncwarp();
+      if (b < kBuckets && (peers & lt_mask) == 0) bv.cur[b] = (uint16_t)(base + __popc(peers));
+      __syncwarp();
     }
-    const unsigned peers = __match_any_sync(FULL, b);
-    int base = 0;
-    if (b < kBuckets) {
-      base = bv.cur[b];
-      bv.pos[base + __popc(peers & lt_mask)] = (uint16_t)s;
-    }
-    __syncwarp();
-    if (b < kBuckets && (peers & lt_mask) == 0) bv.cur[b] = (uint16_t)(base + __popc(peers));
-    __syncwarp();
   }
   // ---- per-bucket range and shifted sums (one lane per bucket, slot order) ----------
 #pragma unroll 1
@@ -685,15 +698,12 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
           }
       }
       __syncwarp();
+      int fcur = 0;  // g grows by 32 per trip: walk the (offset-sorted) flags forward
 #pragma unroll 1
       for (int g = lane; g < total; g += 32) {
         // bucket of flattened member g: last flag with offset <= g
-        int lo = 0, hi = nfl - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if ((int)(bv.flag[mid] >> 8) <= g) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t f = bv.flag[lo];
+        while (fcur + 1 < nfl && (int)(bv.flag[fcur + 1] >> 8) <= g) ++fcur;
+        const uint32_t f = bv.flag[fcur];
         const int b = (int)(f & 0xFFu);
         const int i = bv.off[b] + (g - (int)(f >> 8));
         int lbl = bv.blab[b];
@@ -722,7 +732,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   for (int i = 0; i < NV; ++i) w[i] = 0.0;
   double TA = 0.0;
   const float* B = A + L;
-#pragma unroll 2
+#pragma unroll 4
   for (int i = lane; i < L; i += 32) {
     const int p = bv.pos[i];
     const double ya = (double)__ldg(A + p), yb = (double)__ldg(B + p);
@@ -903,7 +913,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
 // Bucket path (L >= kBucketMinL): kBucketWarps warps per CTA, one query per CTA at a
 // time, one pair per warp at a time (streaming path beyond bucket_lcap).
 template <int G>
-__global__ void __launch_bounds__(kBucketWarps * 32) score_bucket_kernel(ScoreArgs a) {
+__global__ void __launch_bounds__(kBucketWarps * 32, GPOEO_BUCKET_MINB) score_bucket_kernel(ScoreArgs a) {
   __shared__ int64_t s_item;
   __shared__ double s_team[kBucketWarps];
   extern __shared__ __align__(16) uint8_t s_dyn[];  // kBucketWarps x BucketView regions

@@ -37,7 +37,21 @@ __global__ void select_kernel(Plan p, Work w) {
   w.local_lo[t] = (int32_t)lo;
   w.local_hi[t] = (int32_t)hi;
   w.local_base[t] = (int64_t)base;
-  append_items(w.list_b, (int)t, (int)lo, (int)cnt, (int)base);
+  // Alg. 2 on every L of the range, except candidates already scored in phase a4: their
+  // Err(L) is the same deterministic value (same kernel class for the same L), so it is
+  // copied (the oracle memoises identically).
+  int64_t run0 = lo;
+  for (int64_t L = lo; L <= hi + 1; ++L) {
+    int c = -1;
+    if (L <= hi)
+      for (int q = 0; q < nc; ++q)
+        if (w.cand_L[t * p.K + q] == (int32_t)L) c = q;
+    if (c >= 0 || L > hi) {
+      if (L > run0) append_items(w.list_b, (int)t, (int)run0, (int)(L - run0), (int)(base + (run0 - lo)));
+      if (c >= 0) w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
+      run0 = L + 1;
+    }
+  }
 }
 
 // One thread per trace: argmin (Err, L) over the local range -> result (+ detail).

@@ -451,6 +451,8 @@ __constant__ float2 kW32[22] = {
     {-9.238795325e-01f, 3.826834324e-01f}, {-8.314696123e-01f, 5.555702330e-01f}, {-7.071067812e-01f, 7.071067812e-01f},
     {-5.555702330e-01f, 8.314696123e-01f}};
 
+__constant__ float2 kW65536[4] = {{1.000000000e+00f, -0.000000000e+00f}, {9.999999954e-01f, -9.587379910e-05f}, {9.999999816e-01f, -1.917475973e-04f}, {9.999999586e-01f, -2.876213938e-04f}};
+
 // W_16384^m from the quarter table: W^m = (-i)^(m >> 12) * tw[m & 4095]
 __device__ __forceinline__ float2 twiddle(const float2* tw, int m) {
   const float2 b = tw[m & (kTw - 1)];
@@ -648,9 +650,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       const float2 Zp = (q == 0) ? buf[pad((kn2 - k2) & (kn2 - 1))] : buf[pad(kn2 - 1 - k2)];
       const float2 E = make_float2(0.5f * (Zk.x + Zp.x), 0.5f * (Zk.y - Zp.y));
       const float2 O = make_float2(0.5f * (Zk.y + Zp.y), -0.5f * (Zk.x - Zp.x));
-      float s, c;
-      sincospif(-2.0f * (float)k / (float)kN, &s, &c);
-      const float2 X = cadd(E, cmul(make_float2(c, s), O));
+      // W_65536^k = W_16384^(k/4) * W_65536^(k mod 4): table twiddle, no sincos
+      const float2 W = cmul(twiddle(tw, k >> 2), kW65536[k & 3]);
+      const float2 X = cadd(E, cmul(W, O));
       pv[i] = X.x * X.x + X.y * X.y;
     }
     float pnyq = 0.f;
