@@ -447,7 +447,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
                                   long long& passes_out) {
   constexpr int NV = 3 * G + 1;
   constexpr int P = G * (G - 1) / 2;
-  constexpr int KPL = kBuckets / 32;  // buckets per lane
+  constexpr int KPL = kBuckets >= 32 ? kBuckets / 32 : 1;  // buckets per lane (lanes >= K idle if K < 32)
   const unsigned lt_mask = (1u << lane) - 1u;
   // ---- range of W_i ----------------------------------------------------------------
   float mnf = INFINITY, mxf = -INFINITY;
@@ -494,7 +494,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     int run = 0;
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
-      loc[q] = bv.off[lane * KPL + q + 1];
+      loc[q] = (lane * KPL + q < kBuckets) ? bv.off[lane * KPL + q + 1] : 0;
       run += loc[q];
     }
     int incl = run;
@@ -507,8 +507,10 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
-      bv.off[lane * KPL + q] = (uint16_t)base;
-      bv.cur[lane * KPL + q] = (uint16_t)base;
+      if (lane * KPL + q < kBuckets) {
+        bv.off[lane * KPL + q] = (uint16_t)base;
+        bv.cur[lane * KPL + q] = (uint16_t)base;
+      }
       base += loc[q];
     }
     if (lane == 31) bv.off[kBuckets] = (uint16_t)L;
@@ -537,6 +539,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
 #pragma unroll 1
   for (int q = 0; q < KPL; ++q) {
     const int b = lane + 32 * q;
+    if (b >= kBuckets) break;
     const int i0 = bv.off[b], i1 = bv.off[b + 1];
     float lo = INFINITY, hi = -INFINITY, c = 0.f;
     double a1 = 0.0, a2 = 0.0;
@@ -637,6 +640,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     for (int q = 0; q < KPL; ++q) {
       const int b = lane + 32 * q;
       need[q] = 0;
+      if (b >= kBuckets) continue;
       const int cnt = bv.off[b + 1] - bv.off[b];
       if (cnt == 0) continue;
       const double lo = (double)bv.bmin[b] - delta, hi = (double)bv.bmax[b] + delta;
