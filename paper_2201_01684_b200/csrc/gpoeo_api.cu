@@ -289,21 +289,29 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
   gpoeo_result* dres[2] = {reinterpret_cast<gpoeo_result*>(base + 2 * tr),
                            reinterpret_cast<gpoeo_result*>(base + 2 * tr + rs)};
   void* dws[2] = {base + 2 * tr + 2 * rs, base + 2 * tr + 2 * rs + inner};
-  cudaStream_t cs;
-  cudaEvent_t copied[2], done[2];
+  // one copy stream + two compute streams (the caller's and an internal one): chunk c uses
+  // buffer / workspace / stream c & 1, so copies overlap compute and the two chunks in flight
+  // fill each other's phase tails
+  cudaStream_t cs, s2;
+  cudaEvent_t copied[2], done[2], start, fin;
   if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return GPOEO_ERR_CUDA;
+  if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return GPOEO_ERR_CUDA;
+  }
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
   }
-  int rc = GPOEO_OK;
-  // the copy stream must not start before work already queued on `s` that the caller
-  // expects to precede this call
-  cudaEvent_t start;
   cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+  cudaStream_t cst[2] = {s, s2};
+  int rc = GPOEO_OK;
+  // nothing starts before work the caller queued on `s` earlier
   cudaEventRecord(start, s);
   cudaStreamWaitEvent(cs, start, 0);
-  int64_t nchunks = (batch + chunk - 1) / chunk;
+  cudaStreamWaitEvent(s2, start, 0);
+  const int64_t nchunks = (batch + chunk - 1) / chunk;
   for (int64_t c = 0; c < nchunks && rc == GPOEO_OK; ++c) {
     const int b = (int)(c & 1);
     const int64_t first = c * chunk;
@@ -313,16 +321,18 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
                         cudaMemcpyHostToDevice, cs) != cudaSuccess)
       rc = GPOEO_ERR_CUDA;
     cudaEventRecord(copied[b], cs);
-    cudaStreamWaitEvent(s, copied[b], 0);
+    cudaStreamWaitEvent(cst[b], copied[b], 0);
     const Plan pl = make_plan(p, n);
     const Layout L = layout(pl);
-    if (rc == GPOEO_OK) rc = run_detect(dtr[b], pl, L, dws[b], dres[b], nullptr, s);
+    if (rc == GPOEO_OK) rc = run_detect(dtr[b], pl, L, dws[b], dres[b], nullptr, cst[b]);
     if (rc == GPOEO_OK &&
-        cudaMemcpyAsync(host_results + first, dres[b], sizeof(gpoeo_result) * n, cudaMemcpyDeviceToHost, s) !=
+        cudaMemcpyAsync(host_results + first, dres[b], sizeof(gpoeo_result) * n, cudaMemcpyDeviceToHost, cst[b]) !=
             cudaSuccess)
       rc = GPOEO_ERR_CUDA;
-    cudaEventRecord(done[b], s);
+    cudaEventRecord(done[b], cst[b]);
   }
+  cudaEventRecord(fin, s2);
+  cudaStreamWaitEvent(s, fin, 0);
   if (cudaStreamSynchronize(s) != cudaSuccess) rc = GPOEO_ERR_CUDA;
   cudaStreamSynchronize(cs);
   for (int i = 0; i < 2; ++i) {
@@ -330,7 +340,9 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
     cudaEventDestroy(done[i]);
   }
   cudaEventDestroy(start);
+  cudaEventDestroy(fin);
   cudaStreamDestroy(cs);
+  cudaStreamDestroy(s2);
   return rc;
 }
 

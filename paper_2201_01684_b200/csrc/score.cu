@@ -725,8 +725,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     }
     __syncwarp();
     v[3 * G] = (double)changed;
-    xor_sum_vec<NV>(v, 32);
     passes = it;
+    xor_sum_vec<NV>(v, 32);
     if ((it > 1 && v[3 * G] == 0.0) || it == maxit) break;  // labels final
     mstep<G>(cem, v, L, 32, lane);
   }
