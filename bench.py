@@ -98,12 +98,25 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+BACKEND = os.environ.get("GPOEO_DIST_BACKEND", "nccl")  # gloo: code-path test on one GPU
+
+
 def _dist():
     import torch.distributed as dist
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl")
+        dist.init_process_group(BACKEND)
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _max_over_ranks(value: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=dev if BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 # ---------------------------------------------------------------------------------------
@@ -167,6 +180,7 @@ def run_gpu(args) -> None:
     import tracegen as tg
 
     world, rank, local = _dist()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     spec = tg.CFG3.with_(batch=args.batch)
@@ -188,7 +202,12 @@ def run_gpu(args) -> None:
         else:
             g.detect_periods_timed(x, p, ws, res, evs, stream=stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, res)
+            if BACKEND == "nccl":
+                dist.all_gather_into_tensor(gathered, res)  # the only device-to-device transfer
+            else:
+                g_cpu = torch.empty(gathered.shape, dtype=gathered.dtype)
+                dist.all_gather_into_tensor(g_cpu, res.cpu())
+                gathered.copy_(g_cpu)
 
     for _ in range(args.warmup):
         step()
@@ -215,11 +234,7 @@ def run_gpu(args) -> None:
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        tt = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
+    elapsed_ms = _max_over_ranks(t_start.elapsed_time(t_end), dev)
     phases = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)] for evs in phase_evs])  # ms
     phase_ms = phases.mean(axis=0)
 
@@ -285,11 +300,7 @@ def run_gpu(args) -> None:
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             g.detect_periods_host(xh, p, chunk=args.chunk, workspace=hws, out=out)
-        te = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+        te = _max_over_ranks(time.perf_counter() - t0, dev)
         line["e2e"] = {"value": world * Be * args.e2e_steps / te, "unit": "traces/s",
                        "h2d_bytes_per_step": Be * spec.n_features * spec.n_samples * 4,
                        "d2h_bytes_per_step": Be * g.RESULT_DTYPE.itemsize,

@@ -35,6 +35,15 @@ namespace gpoeo {
 #endif
 
 constexpr unsigned FULL = 0xffffffffu;
+
+#ifdef GPOEO_STATS
+// debug build only: [0] bucket pairs, [1] bucket passes, [2] straddling members evaluated,
+// [3] relabelled members, [4] flagged buckets, [5] team pairs, [6] team passes
+__device__ unsigned long long g_stats[8];
+#define GPOEO_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+#else
+#define GPOEO_STAT(i, v) ((void)0)
+#endif
 constexpr int kWarps = kScoreThreads / 32;
 
 template <typename V>
@@ -325,7 +334,7 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
   }
   team_allreduce<NV>(v, tau, team, lane, warp, red, buf);
   if (!clustered) return 0.0;
-  if (lt == 0) passes_out += (long long)(passes + 1) * L;
+  if (lt == 0) { passes_out += (long long)(passes + 1) * L; GPOEO_STAT(5, 1); GPOEO_STAT(6, passes); }
   const double mA = TA / (double)L, mB = v[3 * G] / (double)L;
   double num = 0.0;
 #pragma unroll
@@ -679,6 +688,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       if (lane >= off) incl += o;
     }
     const int total = __shfl_sync(FULL, incl, 31);
+    if (lane == 0) GPOEO_STAT(2, total);
     int changed = 0;
     if (total) {
       // compact flagged buckets in (lane, q) order
@@ -730,6 +740,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     if ((it > 1 && v[3 * G] == 0.0) || it == maxit) break;  // labels final
     mstep<G>(cem, v, L, 32, lane);
   }
+  if (lane == 0) { GPOEO_STAT(0, 1); GPOEO_STAT(1, passes); }
   // ---- final groups on W_i and the same index sets on W_{i+1} (slot order, Z28) -----
   double w[NV];  // nA[G], SA[G], SB[G], TB ; TA separately (same order)
 #pragma unroll
@@ -1037,3 +1048,14 @@ cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, do
 }
 
 }  // namespace gpoeo
+
+#ifdef GPOEO_STATS
+extern "C" __attribute__((visibility("default"))) int gpoeo_debug_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, gpoeo::g_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return -5;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(gpoeo::g_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
