@@ -43,7 +43,10 @@ enum CounterSlot {
   CTR_LOCAL_SLOTS = 9, // local-score slots handed out by select
 };
 
-constexpr int kBucketMinL = 257;  // L >= this: bucketed warp path (score.cu)
+#ifndef GPOEO_BUCKET_MIN_L
+#define GPOEO_BUCKET_MIN_L 513
+#endif
+constexpr int kBucketMinL = GPOEO_BUCKET_MIN_L;  // L >= this: bucketed warp path (score.cu)
 
 // A query list: small-L items packed from the front, the others from the back, so the
 // two scorer kernels (team path / bucketed path) each read one contiguous range.

@@ -180,14 +180,15 @@ __device__ __forceinline__ void mstep(Cem<G>& cem, const double* v, int L, int t
       if (nj == 0.0) {
         c = -INFINITY;  // dead (stays dead)
       } else {
-        const double m = S / nj;
+        const double rn = 1.0 / nj;  // two divisions per component (not five)
+        const double m = S * rn;
         const double dm = m - mu;
-        double var = Q / nj - dm * dm;
+        double var = Q * rn - dm * dm;
         if (var < cem.floor_var) var = cem.floor_var;
-        const double p = nj / (double)L;
-        mu = m;
-        c = 0.5 * log(p * p / var);  // ln pi - 1/2 ln var
         h = 0.5 / var;
+        const double p = nj * (1.0 / (double)L);
+        mu = m;
+        c = 0.5 * log(2.0 * p * p * h);  // ln pi - 1/2 ln var
       }
     }
 #pragma unroll
@@ -377,7 +378,7 @@ constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pair
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
   return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) + (size_t)kBuckets * 8 * 2 +
          (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 2 + (size_t)kBuckets * 4 +
-         kBuckets + 64;
+         (size_t)kBuckets * 32 * 2 + kBuckets + 64;
 }
 
 struct BucketView {
@@ -391,6 +392,7 @@ struct BucketView {
   uint16_t* off;   // [K+1] first slot of bucket b
   uint16_t* cur;   // [K]   scatter cursors
   uint32_t* flag;  // [K]   flagged-bucket list of a pass: (member offset << 8) | bucket
+  uint16_t* lcnt;  // [K][32] per-lane bucket counts / scatter cursors of the counting sort
   uint8_t* blab;   // [K]   whole-bucket label, 0xFF per-sample, 0xFE unset
 
   __device__ static BucketView carve(uint8_t* base, int Lcap) {
@@ -416,6 +418,8 @@ struct BucketView {
     p += (size_t)kBuckets * 2;
     v.flag = reinterpret_cast<uint32_t*>(p);
     p += (size_t)kBuckets * 4;
+    v.lcnt = reinterpret_cast<uint16_t*>(p);
+    p += (size_t)kBuckets * 32 * 2;
     v.blab = p;
     return v;
   }
@@ -457,7 +461,6 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   constexpr int NV = 3 * G + 1;
   constexpr int P = G * (G - 1) / 2;
   constexpr int KPL = kBuckets >= 32 ? kBuckets / 32 : 1;  // buckets per lane (lanes >= K idle if K < 32)
-  const unsigned lt_mask = (1u << lane) - 1u;
   // ---- range of W_i ----------------------------------------------------------------
   float mnf = INFINITY, mxf = -INFINITY;
 #pragma unroll 4
@@ -477,34 +480,34 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // bucket of a value: any deterministic monotone map works (both sort loops use it)
   const float bscale = (float)kBuckets / (mxf - mnf);
   // ---- stable counting sort of sample indices by value bucket ------------------------
-  for (int b = lane; b <= kBuckets; b += 32) bv.off[b] = 0;
-  __syncwarp();
+  // Lane l owns the contiguous chunk [l*CH, (l+1)*CH): per-lane counts cnt[b][l], an
+  // exclusive scan in (bucket, lane) order, then each lane scatters its chunk in order. The
+  // result is sorted by (bucket, position): deterministic, no warp-synchronous multisplit.
   auto bucket_of = [&](int s) -> int {
-    if (s >= L) return kBuckets;
     const int b = (int)((__ldg(A + s) - mnf) * bscale);
     return b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
   };
-#pragma unroll 1
-  for (int s0 = 0; s0 < L; s0 += 128) {
-    int bb[4];
+  const int CH = (L + 31) >> 5;
+  const int c0 = lane * CH, c1 = (c0 + CH < L) ? c0 + CH : L;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) bb[u] = bucket_of(s0 + 32 * u + lane);  // 4 loads in flight
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int b = bb[u];
-      const unsigned peers = __match_any_sync(FULL, b);
-      if (b < kBuckets && (peers & lt_mask) == 0) bv.off[b + 1] += (uint16_t)__popc(peers);
-      __syncwarp();
-    }
+  for (int b = 0; b < kBuckets; ++b) bv.lcnt[b * 32 + lane] = 0;
+#pragma unroll 4
+  for (int s = c0; s < c1; ++s) {
+    const int b = bucket_of(s);
+    bv.lcnt[b * 32 + lane] += 1;  // own column: no race
   }
+  __syncwarp();
   {
-    // exclusive prefix over buckets: lane owns KPL consecutive counters
-    int loc[KPL];
+    // lane b: row total of bucket b, warp exclusive scan, then the row's per-lane offsets
+    int tot[KPL];
     int run = 0;
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
-      loc[q] = (lane * KPL + q < kBuckets) ? bv.off[lane * KPL + q + 1] : 0;
-      run += loc[q];
+      const int b = lane * KPL + q;
+      tot[q] = 0;
+      if (b < kBuckets)
+        for (int l = 0; l < 32; ++l) tot[q] += bv.lcnt[b * 32 + l];
+      run += tot[q];
     }
     int incl = run;
 #pragma unroll
@@ -516,34 +519,29 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
-      if (lane * KPL + q < kBuckets) {
-        bv.off[lane * KPL + q] = (uint16_t)base;
-        bv.cur[lane * KPL + q] = (uint16_t)base;
+      const int b = lane * KPL + q;
+      if (b < kBuckets) {
+        bv.off[b] = (uint16_t)base;
+        int o = base;
+        for (int l = 0; l < 32; ++l) {
+          const int c = bv.lcnt[b * 32 + l];
+          bv.lcnt[b * 32 + l] = (uint16_t)o;
+          o += c;
+        }
       }
-      base += loc[q];
+      base += tot[q];
     }
     if (lane == 31) bv.off[kBuckets] = (uint16_t)L;
     __syncwarp();
   }
-#pragma unroll 1
-  for (int s0 = 0; s0 < L; s0 += 128) {
-    int bb[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) bb[u] = bucket_of(s0 + 32 * u + lane);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int b = bb[u];
-      const unsigned peers = __match_any_sync(FULL, b);
-      int base = 0;
-      if (b < kBuckets) {
-        base = bv.cur[b];
-        bv.pos[base + __popc(peers & lt_mask)] = (uint16_t)(s0 + 32 * u + lane);
-      }
-      __syncwarp();
-      if (b < kBuckets && (peers & lt_mask) == 0) bv.cur[b] = (uint16_t)(base + __popc(peers));
-      __syncwarp();
-    }
+#pragma unroll 4
+  for (int s = c0; s < c1; ++s) {
+    const int b = bucket_of(s);
+    const int slot = bv.lcnt[b * 32 + lane];
+    bv.lcnt[b * 32 + lane] = (uint16_t)(slot + 1);
+    bv.pos[slot] = (uint16_t)s;
   }
+  __syncwarp();
   // ---- per-bucket range and shifted sums (one lane per bucket, slot order) ----------
 #pragma unroll 1
   for (int q = 0; q < KPL; ++q) {
