@@ -321,3 +321,29 @@ def test_full_size_config3_sampled():
     allr = g.results_numpy(res)
     assert set(np.unique(allr["status"])) <= {0, 1}
     assert (allr["period"][allr["status"] == 0] >= spec.min_period).all()
+
+
+def test_similarity_stress_few_levels_and_outliers():
+    # NVML-like coarse quantisation (few distinct values, many exact ties), a lone outlier
+    # that squeezes every other value into one bucket, and a two-level square wave
+    rng = np.random.default_rng(12)
+    N = 8192
+    rows = [
+        np.round(rng.normal(50, 1.5, N)).astype(np.float32),                       # ~10 levels
+        np.where(rng.random(N) < 0.5, 3.0, 7.0).astype(np.float32),                # 2 levels
+        np.concatenate([[1e4], np.round(rng.normal(20, 2, N - 1))]).astype(np.float32),  # outlier
+        (np.where((np.arange(N) % 700) < 300, 10.0, 2.0) + np.round(rng.normal(0, 0.6, N))).astype(np.float32),
+    ]
+    y = np.stack(rows)
+    Ls = [3, 16, 100, 256, 300, 512, 513, 700, 1024, 2000, 4096]
+    ti = np.repeat(np.arange(len(rows)), len(Ls)).astype(np.int32)
+    pe = np.tile(np.array(Ls, np.int32), len(rows))
+    got = g.similarity_error(torch.from_numpy(y).cuda(), ti, pe).cpu().numpy()
+    bad = []
+    for q in range(len(ti)):
+        ref, margin = O.similarity_error(y[ti[q]], int(pe[q]), with_margin=True)
+        if margin < 1e-10:
+            continue
+        if abs(got[q] - ref) > 1e-4 * max(ref, 1e-6):
+            bad.append((int(ti[q]), int(pe[q]), got[q], ref))
+    assert not bad
