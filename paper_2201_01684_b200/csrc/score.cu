@@ -383,7 +383,7 @@ __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
 
 struct BucketView {
   uint16_t* pos;   // [Lcap] sorted slot -> sample index in the window
-  uint8_t* lab;    // [Lcap] label of each sorted slot
+  uint8_t* lab;    // [Lcap] current label of each sample (by position in the window)
   double* s1;      // [K]   sum (y - c_b)
   double* s2;      // [K]   sum (y - c_b)^2
   float* bmin;     // [K]
@@ -719,16 +719,17 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         const int b = (int)(f & 0xFFu);
         const int i = bv.off[b] + (g - (int)(f >> 8));
         int lbl = bv.blab[b];
+        const int p = bv.pos[i];
         if (lbl == 0xFF) {
-          const double y = (double)__ldg(A + bv.pos[i]);
+          const double y = (double)__ldg(A + p);
           double e[G];
           lbl = cem.assign(y, it, e);
 #pragma unroll
           for (int j = 0; j < G; ++j)
             if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
         }
-        changed |= (int)(bv.lab[i] != lbl);
-        bv.lab[i] = (uint8_t)lbl;
+        changed |= (int)(bv.lab[p] != lbl);  // labels are kept per sample position
+        bv.lab[p] = (uint8_t)lbl;
       }
     }
     __syncwarp();
@@ -739,19 +740,19 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     mstep<G>(cem, v, L, 32, lane);
   }
   if (lane == 0) { GPOEO_STAT(0, 1); GPOEO_STAT(1, passes); }
-  // ---- final groups on W_i and the same index sets on W_{i+1} (slot order, Z28) -----
+  // ---- final groups on W_i and the same index sets on W_{i+1} (position order with
+  // coalesced loads; the same loop for both windows, Z28) ------------------------------
   double w[NV];  // nA[G], SA[G], SB[G], TB ; TA separately (same order)
 #pragma unroll
   for (int i = 0; i < NV; ++i) w[i] = 0.0;
   double TA = 0.0;
   const float* B = A + L;
 #pragma unroll 4
-  for (int i = lane; i < L; i += 32) {
-    const int p = bv.pos[i];
+  for (int p = lane; p < L; p += 32) {
     const double ya = (double)__ldg(A + p), yb = (double)__ldg(B + p);
     TA += ya;
     w[3 * G] += yb;
-    const int l = bv.lab[i];
+    const int l = bv.lab[p];
 #pragma unroll
     for (int j = 0; j < G; ++j)
       if (l == j) { w[j] += 1.0; w[G + j] += ya; w[2 * G + j] += yb; }
