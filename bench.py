@@ -242,6 +242,15 @@ def run_gpu(args) -> None:
     peaks, peak_kind = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
 
+    # dram traffic of the dominant kernel from the committed ncu --set full capture
+    traffic, traffic_note = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj["dram_bytes_per_launch"]
+        traffic_note = tj.get("note")
+    except Exception:
+        pass
     # dominant kernel: the Alg. 2 scorer (two launches per step, candidate + local queries)
     score_ms = phase_ms[2] + phase_ms[4]
     passes = counters["cem_sample_passes"]  # per step (samples x CEM passes, incl. the W_{i+1} pass)
@@ -265,7 +274,7 @@ def run_gpu(args) -> None:
         "hbm_frac_end_to_end": (alg_bytes / (elapsed_ms / args.steps / 1e3) / 1e9) / hbm_peak,
         "roofline": {"bound": "alu", "kernel": "score_kernel (Alg. 2 CEM scorer, 2 launches/step)",
                      "achieved": achieved_dp / 1e12, "peak": peak_dp / 1e12, "unit": "TDPinstr/s",
-                     "frac": achieved_dp / peak_dp, "traffic": None,
+                     "frac": achieved_dp / peak_dp, "traffic": traffic, "traffic_note": traffic_note,
                      "work": f"{passes} CEM sample-passes/step x {dp_per_pass} fp64 instr",
                      "peak_note": f"148 SMs x 64 fp64/clk x {sm_max:.0f} MHz (sm_max_mhz, {peak_kind})"},
         "roofline_spectral": {"bound": "hbm", "kernel": "composite + spectrum (a1-a3)",

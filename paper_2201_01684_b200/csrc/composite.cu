@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
     double s = 0.0, q = 0.0;
     if ((N & 3) == 0) {
       const float4* x4 = reinterpret_cast<const float4*>(xc);
+#pragma unroll 8
       for (int i = threadIdx.x; i < N / 4; i += kCompThreads) {
         float4 v = __ldg(x4 + i);
         double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
   if (threadIdx.x == 0) status[t] = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
   float* yt = y + t * (int64_t)N;
   if ((N & 3) == 0) {
+#pragma unroll 4
     for (int i = threadIdx.x; i < N / 4; i += kCompThreads) {
       double v[4] = {0.0, 0.0, 0.0, 0.0};
       for (int c = 0; c < F; ++c) {

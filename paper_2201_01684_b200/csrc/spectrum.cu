@@ -573,9 +573,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       const double x0 = (double)__ldg(xc);
       double s = 0.0, qq = 0.0;
       const float4* x4 = reinterpret_cast<const float4*>(xc);
-      for (int i = threadIdx.x; i < kn2 / 2; i += kT) {  // 2 blocks x 4096 float4
+      // 16 float4 per thread: issue them all before the fp64 math (bytes in flight:
+      // 512 threads x 256 B per SM, enough to cover HBM latency)
+      float4 buf4[kn2 / 2 / kT];
+#pragma unroll
+      for (int u = 0; u < kn2 / 2 / kT; ++u) {
+        const int i = threadIdx.x + u * kT;
         const int blk = (i < kn2 / 4) ? q : 2 + q;
-        const float4 v = __ldg(x4 + blk * (kn2 / 4) + (i & (kn2 / 4 - 1)));
+        buf4[u] = __ldg(x4 + blk * (kn2 / 4) + (i & (kn2 / 4 - 1)));
+      }
+#pragma unroll
+      for (int u = 0; u < kn2 / 2 / kT; ++u) {
+        const float4 v = buf4[u];
         const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
         s += v0; s += v1; s += v2; s += v3;
         const double d0 = v0 - x0, d1 = v1 - x0, d2 = v2 - x0, d3 = v3 - x0;
@@ -609,6 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     }
     // ---- a1 signal + DIF split into the two CTAs' buffers ------------------------------
     float* yt = y_out + t * (int64_t)kN;
+#pragma unroll 4
     for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
       const int j = q * (kn2 / 2) + jj;
       double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
