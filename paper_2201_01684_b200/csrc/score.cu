@@ -37,8 +37,8 @@ namespace gpoeo {
 constexpr unsigned FULL = 0xffffffffu;
 
 #ifdef GPOEO_STATS
-// debug build only: [0] bucket pairs, [1] bucket passes, [2] straddling members evaluated,
-// [3] relabelled members, [4] flagged buckets, [5] team pairs, [6] team passes
+// debug build only: [0] bucket pairs, [1] bucket passes, [2] members swept (straddling +
+// relabelled), [3] straddling members, [4] straddling buckets, [5] team pairs, [6] team passes
 __device__ unsigned long long g_stats[8];
 #define GPOEO_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
@@ -378,7 +378,7 @@ constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pair
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
   return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) + (size_t)kBuckets * 8 * 2 +
          (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 2 + (size_t)kBuckets * 4 +
-         (size_t)kBuckets * 32 * 2 + kBuckets + 64;
+         (size_t)kBuckets * 32 * 2 + kBuckets + (size_t)kBuckets * 4 + 64;
 }
 
 struct BucketView {
@@ -393,7 +393,8 @@ struct BucketView {
   uint16_t* cur;   // [K]   scatter cursors
   uint32_t* flag;  // [K]   flagged-bucket list of a pass: (member offset << 8) | bucket
   uint16_t* lcnt;  // [K][32] per-lane bucket counts / scatter cursors of the counting sort
-  uint8_t* blab;   // [K]   whole-bucket label, 0xFF per-sample, 0xFE unset
+  uint8_t* blab;   // [K]   bucket state: l < G every member has label l; 0xFF mixed (lab[]); 0xFE unset
+  uint32_t* seen;  // [K]   labels seen among a straddling bucket's members this pass (bit mask)
 
   __device__ static BucketView carve(uint8_t* base, int Lcap) {
     BucketView v;
@@ -421,6 +422,8 @@ struct BucketView {
     v.lcnt = reinterpret_cast<uint16_t*>(p);
     p += (size_t)kBuckets * 32 * 2;
     v.blab = p;
+    p += ((size_t)kBuckets + 3) & ~(size_t)3;
+    v.seen = reinterpret_cast<uint32_t*>(p);
     return v;
   }
 };
@@ -483,10 +486,11 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // Lane l owns the contiguous chunk [l*CH, (l+1)*CH): per-lane counts cnt[b][l], an
   // exclusive scan in (bucket, lane) order, then each lane scatters its chunk in order. The
   // result is sorted by (bucket, position): deterministic, no warp-synchronous multisplit.
-  auto bucket_of = [&](int s) -> int {
-    const int b = (int)((__ldg(A + s) - mnf) * bscale);
+  auto bucket_of_v = [&](float v) -> int {
+    const int b = (int)__fmul_rn(__fsub_rn(v, mnf), bscale);
     return b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
   };
+  auto bucket_of = [&](int s) -> int { return bucket_of_v(__ldg(A + s)); };
   const int CH = (L + 31) >> 5;
   const int c0 = lane * CH, c1 = (c0 + CH < L) ? c0 + CH : L;
 #pragma unroll
@@ -574,75 +578,91 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   Cem<G> cem;
   cem.init(mn, R);
   const double delta = 1e-6 * R;
-  // pair of components solved by this lane (lane < P)
-  int pj = 0, pk = 1;
-  {
+  // root slot x = lane + 32 t (t < RPL) is root (x & 1) of component pair x >> 1
+  constexpr int RPL = (2 * P + 31) / 32 > 0 ? (2 * P + 31) / 32 : 1;
+  int pj[RPL], pk[RPL];
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) {
+    pj[t] = 0;
+    pk[t] = 1;
     int cntp = 0;
 #pragma unroll
     for (int j = 0; j < G; ++j)
 #pragma unroll
       for (int k = j + 1; k < G; ++k) {
-        if (cntp == lane) { pj = j; pk = k; }
+        if (cntp == ((lane + 32 * t) >> 1)) { pj[t] = j; pk[t] = k; }
         ++cntp;
       }
   }
   int passes = 0;
 #pragma unroll 1
   for (int it = 1; it <= maxit; ++it) {
-    // crossings of every live pair: lane p < P solves pair p, then broadcast
-    double rt[2 * (P > 0 ? P : 1)];
-    {
+    // crossings of every live pair: the even slot of a pair solves it (both roots), the odd
+    // slot takes the second root; each slot then drops its root if a third component
+    // clearly beats both there (such a crossing is not on the upper envelope and changes
+    // no label; the margin absorbs root rounding)
+    double r[RPL];
+    unsigned vmask[RPL];
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int x = lane + 32 * t;
       double r0 = NAN, r1 = NAN;
-      if (lane < P) {
-        double muj = 0, cj = 0, hj = 0, muk = 0, ck = 0, hk = 0;
+      double muj = 0, cj = 0, hj = 0, muk = 0, ck = 0, hk = 0;
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          if (j == pj) { muj = cem.mu[j]; cj = cem.c[j]; hj = cem.h[j]; }
-          if (j == pk) { muk = cem.mu[j]; ck = cem.c[j]; hk = cem.h[j]; }
-        }
-        if (it == 1) { cj = ck = 0.0; hj = hk = 1.0; }  // first pass: argmin (y - mu)^2
-        score_crossings(muj, cj, hj, muk, ck, hk, mn, r0, r1);
-        // keep only crossings on the upper envelope: if a third component beats both
-        // clearly at the crossing, the winner there is that component and the pair's
-        // crossing cannot change any label (the margin absorbs root rounding).
+      for (int j = 0; j < G; ++j) {
+        if (j == pj[t]) { muj = cem.mu[j]; cj = cem.c[j]; hj = cem.h[j]; }
+        if (j == pk[t]) { muk = cem.mu[j]; ck = cem.c[j]; hk = cem.h[j]; }
+      }
+      if (it == 1) { cj = ck = 0.0; hj = hk = 1.0; }  // first pass: argmin (y - mu)^2
+      if (x < 2 * P && (x & 1) == 0) score_crossings(muj, cj, hj, muk, ck, hk, mn, r0, r1);
+      const double r1_left = __shfl_up_sync(FULL, r1, 1);
+      r[t] = (x & 1) ? r1_left : r0;
+      bool valid = (x < 2 * P) && (r[t] == r[t]);
+      if (valid) {
+        const double d = r[t] - muj;
+        const double sj = cj - hj * d * d;
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-          const double r = rr ? r1 : r0;
-          if (r != r) continue;  // NaN: no root
-          double sj;
-          if (it == 1) {
-            const double d = r - muj;
-            sj = -d * d;
-          } else {
-            const double d = r - muj;
-            sj = cj - hj * d * d;
-          }
-          bool dominated = false;
-#pragma unroll
-          for (int m = 0; m < G; ++m) {
-            if (m == pj || m == pk) continue;
-            double sm;
-            const double d = r - cem.mu[m];
-            if (it == 1) sm = -d * d;
-            else sm = cem.c[m] == -INFINITY ? -INFINITY : cem.c[m] - cem.h[m] * d * d;
-            dominated |= sm > sj + 1e-6 * (fabs(sj) + fabs(sm) + 1.0);
-          }
-          if (dominated) {
-            if (rr) r1 = NAN; else r0 = NAN;
-          }
+        for (int m = 0; m < G; ++m) {
+          if (m == pj[t] || m == pk[t]) continue;
+          const double dm = r[t] - cem.mu[m];
+          double sm;
+          if (it == 1) sm = -dm * dm;
+          else sm = cem.c[m] == -INFINITY ? -INFINITY : cem.c[m] - cem.h[m] * dm * dm;
+          valid &= !(sm > sj + 1e-6 * (fabs(sj) + fabs(sm) + 1.0));
         }
       }
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        rt[2 * p] = __shfl_sync(FULL, r0, p);
-        rt[2 * p + 1] = __shfl_sync(FULL, r1, p);
-      }
+      vmask[t] = __ballot_sync(FULL, valid);
     }
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;
-    // classify this lane's buckets; count members that need per-slot work
+    // classify this lane's buckets. A bucket with no envelope root within
+    // [min - delta, max + delta] is whole: every member takes the label of the per-sample
+    // rule at its minimum, statistics from the bucket sums. Its state records that label;
+    // a state change is a label change of every member (mixed -> whole always changes one).
+    bool stq[KPL];
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) stq[q] = false;
+    {
+      double lo[KPL], hi[KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) {
+        const int b = lane + 32 * q;
+        lo[q] = b < kBuckets ? (double)bv.bmin[b] - delta : 1.0;
+        hi[q] = b < kBuckets ? (double)bv.bmax[b] + delta : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+#pragma unroll 1
+        for (unsigned m = vmask[t]; m; m &= m - 1) {
+          const double rr = __shfl_sync(FULL, r[t], __ffs(m) - 1);
+#pragma unroll
+          for (int q = 0; q < KPL; ++q) stq[q] |= (rr >= lo[q]) & (rr <= hi[q]);
+        }
+      }
+    }
     int need[KPL];
+    int changed = 0;
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
       const int b = lane + 32 * q;
@@ -650,13 +670,11 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       if (b >= kBuckets) continue;
       const int cnt = bv.off[b + 1] - bv.off[b];
       if (cnt == 0) continue;
-      const double lo = (double)bv.bmin[b] - delta, hi = (double)bv.bmax[b] + delta;
-      bool st = false;
-#pragma unroll
-      for (int r = 0; r < 2 * P; ++r) st |= (rt[r] >= lo) & (rt[r] <= hi);
-      if (st) {
-        bv.blab[b] = 0xFF;
+      if (stq[q]) {
         need[q] = cnt;
+        bv.seen[b] = 0u;
+        GPOEO_STAT(3, cnt);
+        GPOEO_STAT(4, 1);
         continue;
       }
       double e[G];
@@ -670,12 +688,10 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
           v[G + j] += n * c + a1;
           v[2 * G + j] += a2 + dc * (2.0 * a1 + n * dc);
         }
-      if (bv.blab[b] != lbl) {
-        bv.blab[b] = (uint8_t)lbl;
-        need[q] = cnt;
-      }
+      changed |= (int)(bv.blab[b] != lbl);  // 0xFF (mixed) -> l changes some member
+      bv.blab[b] = (uint8_t)lbl;
     }
-    // flattened list of flagged buckets: (exclusive member offset << 8) | bucket
+    // flattened member list of the straddling buckets: (exclusive member offset << 8) | bucket
     int mine = 0;
 #pragma unroll
     for (int q = 0; q < KPL; ++q) mine += need[q];
@@ -687,9 +703,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     }
     const int total = __shfl_sync(FULL, incl, 31);
     if (lane == 0) GPOEO_STAT(2, total);
-    int changed = 0;
     if (total) {
-      // compact flagged buckets in (lane, q) order
       int myfl = 0;
 #pragma unroll
       for (int q = 0; q < KPL; ++q) myfl += need[q] != 0;
@@ -713,24 +727,32 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       int fcur = 0;  // g grows by 32 per trip: walk the (offset-sorted) flags forward
 #pragma unroll 1
       for (int g = lane; g < total; g += 32) {
-        // bucket of flattened member g: last flag with offset <= g
         while (fcur + 1 < nfl && (int)(bv.flag[fcur + 1] >> 8) <= g) ++fcur;
         const uint32_t f = bv.flag[fcur];
         const int b = (int)(f & 0xFFu);
         const int i = bv.off[b] + (g - (int)(f >> 8));
-        int lbl = bv.blab[b];
         const int p = bv.pos[i];
-        if (lbl == 0xFF) {
-          const double y = (double)__ldg(A + p);
-          double e[G];
-          lbl = cem.assign(y, it, e);
+        const double y = (double)__ldg(A + p);
+        double e[G];
+        const int lbl = cem.assign(y, it, e);
 #pragma unroll
-          for (int j = 0; j < G; ++j)
-            if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
-        }
-        changed |= (int)(bv.lab[p] != lbl);  // labels are kept per sample position
+        for (int j = 0; j < G; ++j)
+          if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
+        const int st = bv.blab[b];  // previous state: uniform label, or mixed (per member)
+        const int old = st < G ? st : (int)bv.lab[p];
+        changed |= (int)(old != lbl);
         bv.lab[p] = (uint8_t)lbl;
+        atomicOr(&bv.seen[b], 1u << lbl);
       }
+      __syncwarp();
+      // new state of each straddling bucket: uniform label, or mixed
+#pragma unroll
+      for (int q = 0; q < KPL; ++q)
+        if (need[q]) {
+          const int b = lane + 32 * q;
+          const uint32_t sm = bv.seen[b];
+          bv.blab[b] = (uint8_t)((sm & (sm - 1)) ? 0xFF : (__ffs(sm) - 1));
+        }
     }
     __syncwarp();
     v[3 * G] = (double)changed;
@@ -741,7 +763,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   }
   if (lane == 0) { GPOEO_STAT(0, 1); GPOEO_STAT(1, passes); }
   // ---- final groups on W_i and the same index sets on W_{i+1} (position order with
-  // coalesced loads; the same loop for both windows, Z28) ------------------------------
+  // coalesced loads; the same loop for both windows, Z28). A sample's final label is its
+  // bucket's state, or its own label when the bucket is mixed. -------------------------
   double w[NV];  // nA[G], SA[G], SB[G], TB ; TA separately (same order)
 #pragma unroll
   for (int i = 0; i < NV; ++i) w[i] = 0.0;
@@ -749,10 +772,12 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   const float* B = A + L;
 #pragma unroll 4
   for (int p = lane; p < L; p += 32) {
-    const double ya = (double)__ldg(A + p), yb = (double)__ldg(B + p);
+    const float fa = __ldg(A + p);
+    const double ya = (double)fa, yb = (double)__ldg(B + p);
     TA += ya;
     w[3 * G] += yb;
-    const int l = bv.lab[p];
+    int l = bv.blab[bucket_of_v(fa)];
+    if (l >= G) l = bv.lab[p];
 #pragma unroll
     for (int j = 0; j < G; ++j)
       if (l == j) { w[j] += 1.0; w[G + j] += ya; w[2 * G + j] += yb; }
