@@ -73,6 +73,12 @@ class OrResult(ctypes.Structure):
     ]
 
 
+class OrMajor(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("period", ctypes.c_int32), ("bin", ctypes.c_int32),
+                ("n_peaks", ctypes.c_int32), ("period_s", ctypes.c_double), ("power", ctypes.c_double),
+                ("d_major", ctypes.c_double), ("d_peak", ctypes.c_double)]
+
+
 def build() -> str:
     """Compile the oracle (gcc, fp64, no FMA contraction). Building the checker is not using it."""
     if not (os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC)):
@@ -109,6 +115,9 @@ def _L():
         lib.oracle_exhaustive.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, P]
         lib.oracle_exhaustive.restype = ctypes.c_int32
+        lib.oracle_major.argtypes = [P, ctypes.POINTER(OrParams), P, ctypes.POINTER(OrMajor)]
+        lib.oracle_major.restype = ctypes.c_int
+        assert lib.oracle_sizeof_major() == ctypes.sizeof(OrMajor)
         assert lib.oracle_sizeof_params() == ctypes.sizeof(OrParams)
         assert lib.oracle_sizeof_result() == ctypes.sizeof(OrResult)
         _lib = lib
@@ -290,3 +299,38 @@ def exhaustive(y: np.ndarray, min_period: int, max_period: int, num_groups: int 
     errs = np.empty(max_period - min_period + 1)
     L = _L().oracle_exhaustive(_ptr(y), y.size, min_period, max_period, num_groups, max_iters, _ptr(errs))
     return L, errs
+
+
+@dataclass
+class Major:
+    """S1 spectral-only result (T_iter = 1/f_major; reading R3)."""
+    status: int
+    period: int
+    bin: int
+    period_s: float
+    power: float
+    n_peaks: int
+    d_major: float
+    d_peak: float
+
+    def ambiguous(self, thr_spec=1e-4) -> bool:
+        """Z27: the fp32 FFT may order two peaks within thr_spec of P_major either way."""
+        return self.d_major < thr_spec or self.d_peak < thr_spec
+
+
+def major(x: np.ndarray, params: Params) -> Major:
+    """S1 on one trace x float32 [F][N]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    p = params.c()
+    m = OrMajor()
+    w = None if params.weights is None else np.asarray(params.weights, np.float32).astype(np.float64)
+    if _L().oracle_major(_ptr(x), ctypes.byref(p), None if w is None else _ptr(w), ctypes.byref(m)) != 0:
+        raise ValueError("oracle_major: invalid parameters")
+    return Major(status=m.status, period=m.period, bin=m.bin, period_s=m.period_s, power=m.power,
+                 n_peaks=m.n_peaks, d_major=m.d_major, d_peak=m.d_peak)
+
+
+def major_batch(X: np.ndarray, params: Params, threads: int | None = None) -> list[Major]:
+    threads = threads or os.cpu_count() or 1
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(lambda b: major(X[b], params), range(X.shape[0])))

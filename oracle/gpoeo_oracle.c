@@ -24,6 +24,7 @@
  *   O7 final argmin                             Alg.1 l.18-19, P:329-331 (+ Z17, Z20)
  *   O8 margins (Z27) and work counters
  *   O9 exhaustive search (tests only)
+ *   S1 spectral-only detector (T_iter = 1/f_major)
  *
  * Pins (tests/test_oracle_*.py): O1 closed-form z-scores; O2 numpy.fft.rfft,
  * Parseval, pure tones, impulse; O3 hand spectra and scipy find_peaks;
@@ -505,6 +506,90 @@ done:
   free(P);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* S1. Spectral-only detector (the Fourier-transform method of
+ * section 4.1.1, ODPP's detector P:159-161): "The one with the largest
+ * amplitude is the major frequency component. The iterative period T_iter can be
+ * calculated as T_iter = 1/f_major". Reading R3: the major
+ * component is the in-band spectral peak (Z5 peak rule, Z21 band, Z7) with the largest
+ * P_k = |X_k|^2 (Z3), ties to the smaller k (the (P desc, k asc) order of Z8); the
+ * integer period is floor(N/k) (Z9), in seconds floor(N/k) * T_s (Z20). Status as
+ * Alg. 1: CONSTANT (O1), INSUFFICIENT (empty band), APERIODIC (no in-band peak).
+ * Margins (Z27): d_major = (P_major - P_second) / P_major over the in-band peaks,
+ * d_peak = min |P_major - P_{major +- 1}| / P_major. */
+typedef struct {
+  int32_t status;
+  int32_t period;
+  int32_t bin;
+  int32_t n_peaks;
+  double period_s;
+  double power;
+  double d_major;
+  double d_peak;
+} or_major;
+
+int oracle_major(const float* x, const or_params* p, const double* weights, or_major* m) {
+  memset(m, 0, sizeof(*m));
+  const int32_t N = p->n_samples;
+  if (N < 8 || p->n_features < 1 || p->n_features > 8 || p->min_period < 2 || p->max_period < p->min_period ||
+      p->max_period > N / 2)
+    return -1;
+  m->period = -1;
+  m->bin = -1;
+  m->d_major = m->d_peak = INFINITY;
+  float* y = (float*)malloc(sizeof(float) * N);
+  double* P = (double*)malloc(sizeof(double) * (N / 2 + 1));
+  /* O1 */
+  if (oracle_composite(x, N, p->n_features, weights, y, NULL, NULL)) { m->status = OR_TRACE_CONSTANT; goto done; }
+  int32_t k0 = N, k1 = 0;
+  for (int64_t k = 1; k <= N / 2; ++k)
+    if (in_band(N, k, p->min_period, p->max_period)) {
+      if (k < k0) k0 = (int32_t)k;
+      if (k > k1) k1 = (int32_t)k;
+    }
+  if (k1 < k0) { m->status = OR_TRACE_INSUFFICIENT; goto done; }
+  /* O2, at every bin the peak test reads */
+  if (p->dft_band_only) {
+    for (int k = 0; k <= N / 2; ++k) P[k] = NAN;
+    int32_t a = k0 - 1 < 0 ? 0 : k0 - 1, b = k1 + 1 > N / 2 ? N / 2 : k1 + 1;
+    oracle_power_spectrum_range(y, N, a, b, P);
+    if (b == N / 2 && N / 2 - 1 < a) oracle_power_spectrum_range(y, N, N / 2 - 1, N / 2 - 1, P);
+  } else {
+    oracle_power_spectrum(y, N, P);
+  }
+  /* the largest in-band peak, scanning k upwards with a strict comparison (ties keep the
+   * smaller k) */
+  int32_t kb = -1;
+  double pb = 0.0, second = -1.0;
+  for (int64_t k = k0; k <= k1; ++k) {
+    if (!(P[k] > mirrored(P, N, k - 1) && P[k] >= mirrored(P, N, k + 1))) continue;
+    m->n_peaks++;
+    if (kb < 0 || P[k] > pb) {
+      if (kb >= 0) second = pb;
+      kb = (int32_t)k;
+      pb = P[k];
+    } else if (P[k] > second) {
+      second = P[k];
+    }
+  }
+  if (kb < 0) { m->status = OR_TRACE_APERIODIC; goto done; }
+  m->bin = kb;
+  m->power = pb;
+  m->period = N / kb;
+  m->period_s = (double)m->period * p->sample_interval;
+  m->status = OR_TRACE_OK;
+  if (second >= 0.0) m->d_major = (pb - second) / pb;
+  {
+    double a = fabs(pb - mirrored(P, N, kb - 1)) / pb, b = fabs(pb - mirrored(P, N, kb + 1)) / pb;
+    m->d_peak = a < b ? a : b;
+  }
+done:
+  free(y);
+  free(P);
+  return 0;
+}
+int oracle_sizeof_major(void) { return (int)sizeof(or_major); }
 
 /* O9 (tests only): Err(L) for every L in [L_min, L_max] of an already-formed
  * signal y; returns the global argmin (Err, L). */
