@@ -162,6 +162,32 @@ int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples
                            const int32_t* period, int64_t n_queries, int32_t num_groups, int32_t gmm_max_iters,
                            double* error_out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Spectral-only detector ----------------------------------------
+ * The Fourier-transform period of section 4.1.1, ODPP's detector:
+ * "the one with the largest amplitude is the major frequency component ... T_iter =
+ * 1/f_major". Reading R3: f_major is the in-band spectral peak (the
+ * Z5 peak rule over the Z21 band, Z7) with the largest P_k = |X_k|^2 of the composite
+ * signal (Z1-Z4), ties to the smaller k; the integer period is floor(N/k) (Z9). Rows a1-a3
+ * of Alg. 1 plus an arg-max: no Alg. 2. Parameters used: n_samples, n_features,
+ * trace_stride, sample_interval, min/max_period, feature_weights (the others are validated
+ * but unused). Per-trace status as Alg. 1 (CONSTANT, INSUFFICIENT, APERIODIC). 16 bytes. */
+typedef struct {
+  int32_t period;   /* floor(N / k_major) samples; -1 if none                            */
+  float period_s;   /* period * T_s [s]                                                  */
+  int32_t bin;      /* k_major; -1 if none                                               */
+  int32_t status;   /* gpoeo_trace_status                                                */
+} gpoeo_major_result;
+
+/* Workspace bytes for gpoeo_detect_major_periods (HOST, pure; 0 if *p is invalid). For
+ * N = 65536 with F <= 3 one fused kernel reads each trace once and keeps everything on
+ * chip (256 B); otherwise the composite signal y[B][N] and statuses live here. */
+size_t gpoeo_major_workspace_size(const gpoeo_params* p, int64_t batch);
+
+/* Spectral-only detection over a batch. traces as gpoeo_detect_periods; results [batch]
+ * gpoeo_major_result (device), written once per trace. Asynchronous, allocation-free. */
+int gpoeo_detect_major_periods(const float* traces, int64_t batch, const gpoeo_params* p,
+                               gpoeo_major_result* results, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Work counters of the last device-pointer call that used `workspace` (HOST read after
  * the caller synchronised): number of Alg.2 queries and CEM sample-passes. Used by
  * bench.py to report ALU roofline numbers. Returns GPOEO_OK. */

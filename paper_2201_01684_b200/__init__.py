@@ -48,7 +48,8 @@ DETAIL_DTYPE = np.dtype([("n_candidates", "<i4"), ("best_bin", "<i4"), ("local_l
                          ("cand_k", "<i4", (MAX_CANDIDATES,)), ("cand_L", "<i4", (MAX_CANDIDATES,)),
                          ("cand_P", "<f4", (MAX_CANDIDATES,)), ("cand_err", "<f8", (MAX_CANDIDATES,)),
                          ("best_err", "<f8")])
-assert RESULT_DTYPE.itemsize == 24 and DETAIL_DTYPE.itemsize == 664
+MAJOR_DTYPE = np.dtype([("period", "<i4"), ("period_s", "<f4"), ("bin", "<i4"), ("status", "<i4")])
+assert RESULT_DTYPE.itemsize == 24 and DETAIL_DTYPE.itemsize == 664 and MAJOR_DTYPE.itemsize == 16
 
 _lib = None
 
@@ -98,6 +99,10 @@ def load():
     lib.gpoeo_similarity_error.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, P, ctypes.c_int64, ctypes.c_int32,
                                            ctypes.c_int32, P, P, ctypes.c_size_t, P]
     lib.gpoeo_similarity_error.restype = ctypes.c_int
+    lib.gpoeo_major_workspace_size.argtypes = [PP, ctypes.c_int64]
+    lib.gpoeo_major_workspace_size.restype = ctypes.c_size_t
+    lib.gpoeo_detect_major_periods.argtypes = [P, ctypes.c_int64, PP, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_detect_major_periods.restype = ctypes.c_int
     lib.gpoeo_read_counters.argtypes = [P, PP, ctypes.c_int64, ctypes.POINTER(GpoeoCounters), P]
     lib.gpoeo_read_counters.restype = ctypes.c_int
     lib.gpoeo_status_string.argtypes = [ctypes.c_int]
@@ -259,6 +264,36 @@ def similarity_error(signal, trace_index, period, num_groups: int = 4, gmm_max_i
                                     _stream_handle(stream))
     _check(rc, "gpoeo_similarity_error")
     return out
+
+
+def major_workspace_size(p: GpoeoParams, batch: int) -> int:
+    return int(load().gpoeo_major_workspace_size(ctypes.byref(p), batch))
+
+
+def detect_major_periods(traces, p: GpoeoParams, workspace=None, results=None, stream=None):
+    """Spectral-only detector (T_iter = 1/f_major; reading R3) on a CUDA float32
+    tensor of traces [B][trace_stride]. Returns (results uint8 tensor of MAJOR_DTYPE
+    records, workspace). Asynchronous on `stream`."""
+    import torch
+    assert traces.is_cuda and traces.dtype == torch.float32 and traces.is_contiguous()
+    B = traces.shape[0]
+    lib = load()
+    need = major_workspace_size(p, B)
+    if need == 0:
+        _check(validate(p), "params")
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, traces.device)
+    if results is None:
+        results = torch.empty(B * MAJOR_DTYPE.itemsize, dtype=torch.uint8, device=traces.device)
+    rc = lib.gpoeo_detect_major_periods(ctypes.c_void_p(traces.data_ptr()), B, ctypes.byref(p),
+                                        ctypes.c_void_p(results.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+                                        workspace.numel(), _stream_handle(stream))
+    _check(rc, "gpoeo_detect_major_periods")
+    return results, workspace
+
+
+def major_numpy(results) -> np.ndarray:
+    return results.cpu().numpy().view(MAJOR_DTYPE)
 
 
 def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:

@@ -147,6 +147,7 @@ Work carve(const Plan& pl, const Layout& L, void* ws) {
                       &w.ctr[CTR_B_BIG], &w.ctr[CTR_CUR_B_SMALL], &w.ctr[CTR_CUR_B_BIG]};
   w.local_err = reinterpret_cast<double*>(b + L.off_lerr);
   w.lab_scratch = L.lab_stride ? reinterpret_cast<uint8_t*>(b + L.off_lab) : nullptr;
+  w.major = nullptr;
   return w;
 }
 
@@ -177,8 +178,8 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   if (pl.batch > 0 && !fused) CK(launch_composite(traces, pl, w.y, w.status, s));
   CK(mark(1));
   if (pl.batch > 0) {
-    if (fused) CK(launch_spectral_fused(pl, traces, w, w.y, nullptr, true, s));
-    else CK(launch_spectrum(pl, w.y, w.status, w, nullptr, true, s));
+    if (fused) CK(launch_spectral_fused(pl, traces, w, w.y, nullptr, kPeaksCandidates, s));
+    else CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
   }
   CK(mark(2));
   if (pl.batch > 0)
@@ -363,11 +364,47 @@ int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params*
   if (batch == 0) return GPOEO_OK;
   float* y = signal ? signal : w.y;
   if (pl.N == 65536 && pl.F <= 3) {
-    CK(launch_spectral_fused(pl, traces, w, y, spectra, false, s));
+    CK(launch_spectral_fused(pl, traces, w, y, spectra, kPeaksNone, s));
     return GPOEO_OK;
   }
   CK(launch_composite(traces, pl, y, w.status, s));
-  if (spectra) CK(launch_spectrum(pl, y, w.status, w, spectra, false, s));
+  if (spectra) CK(launch_spectrum(pl, y, w.status, w, spectra, kPeaksNone, s));
+  return GPOEO_OK;
+}
+
+// Spectral-only detector: rows a1-a3 + arg-max, reading R3.
+static bool major_fused(const gpoeo_params* p) { return p->n_samples == 65536 && p->n_features <= 3; }
+
+size_t gpoeo_major_workspace_size(const gpoeo_params* p, int64_t batch) {
+  if (validate(p) != GPOEO_OK || batch < 0) return 0;
+  if (major_fused(p)) return kAlign;
+  return align_up(sizeof(float) * (size_t)batch * (size_t)p->n_samples) + align_up(sizeof(int32_t) * (size_t)batch);
+}
+
+int gpoeo_detect_major_periods(const float* traces, int64_t batch, const gpoeo_params* p,
+                               gpoeo_major_result* results, void* workspace, size_t workspace_bytes, void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!traces || !results)) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < gpoeo_major_workspace_size(p, batch)) return GPOEO_ERR_WORKSPACE;
+  if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  if (batch == 0) return GPOEO_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Plan pl = make_plan(p, batch);
+  Work w;
+  memset(&w, 0, sizeof(w));
+  w.major = results;
+  if (major_fused(p)) {
+    CK(launch_spectral_fused(pl, traces, w, nullptr, nullptr, kPeaksMajor, s));
+    return GPOEO_OK;
+  }
+  char* b = static_cast<char*>(workspace);
+  w.y = reinterpret_cast<float*>(b);
+  w.status = reinterpret_cast<int32_t*>(b + align_up(sizeof(float) * (size_t)batch * (size_t)p->n_samples));
+  CK(launch_composite(traces, pl, w.y, w.status, s));
+  CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksMajor, s));
   return GPOEO_OK;
 }
 

@@ -99,15 +99,20 @@ struct Work {
   double* local_err;        // [B*max_local]
   uint8_t* lab_scratch;     // warp-mode label scratch for L > kLabCap (may be null)
   unsigned long long* ctr;  // [kCounterSlots]
+  gpoeo_major_result* major;  // spectral-only results (mode kPeaksMajor), else null
 };
+
+// What the spectral kernels do after the power spectrum.
+enum PeakMode { kPeaksNone = 0, kPeaksCandidates = 1, kPeaksMajor = 2 };
 
 // Launchers (each returns cudaGetLastError()).
 cudaError_t launch_composite(const float* x, const Plan& p, float* y, int32_t* status, cudaStream_t s);
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
-                            bool find_peaks, cudaStream_t s);
+                            int mode, cudaStream_t s);
 // Fused a1 + a2 + a3 (N = 65536 only): composite, spectrum and candidates in one kernel.
+// y_out may be null (spectral-only: nothing but the results leaves the chip).
 cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
-                                  bool find_peaks, cudaStream_t s);
+                                  int mode, cudaStream_t s);
 cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
                          int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);

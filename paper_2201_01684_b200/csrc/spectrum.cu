@@ -283,10 +283,55 @@ __device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, in
 
 }
 
+// Spectral-only detector (reading R3): the in-band peak with the largest P, ties
+// to the smaller k, -> period floor(N/k). Called by the whole CTA of cluster rank 0.
+template <int C, int T>
+__device__ void find_major(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, gpoeo_major_result* out,
+                           PeakShared& ps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = T / 32;
+  float bp = -1.f;
+  int32_t bk = 0x7fffffff;
+  for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {  // k increases: strict > keeps the smaller k
+    const float pk = Pv(k);
+    if (pk > Pv(k - 1) && pk >= Pv(k + 1) && pk > bp) { bp = pk; bk = (int32_t)k; }
+  }
+  for (int off = 16; off; off >>= 1) {
+    const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+    const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+    if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+  }
+  if (lane == 0) { ps.redP[warp] = bp; ps.redk[warp] = bk; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < NW; ++i) {
+      const float op = ps.redP[i];
+      const int32_t ok = ps.redk[i];
+      if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+    }
+    int32_t status = st;
+    if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;  // empty band (Z21)
+    if (status == GPOEO_TRACE_OK && bp < 0.f) status = GPOEO_TRACE_APERIODIC;
+    gpoeo_major_result r;
+    r.status = status;
+    if (status == GPOEO_TRACE_OK) {
+      r.bin = bk;
+      r.period = p.N / bk;
+      r.period_s = (float)((double)r.period * p.Ts);
+    } else {
+      r.bin = -1;
+      r.period = -1;
+      r.period_s = -1.f;
+    }
+    out[t] = r;
+  }
+  __syncthreads();
+}
+
 template <int LOGN2, int C>
 __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, const float* __restrict__ y,
                                                                     const int32_t* __restrict__ status_in, Work w,
-                                                                    float* __restrict__ spectra, int find_peaks) {
+                                                                    float* __restrict__ spectra, int mode) {
   using Cfg = SpecCfg<LOGN2>;
   constexpr int T = Cfg::T;
   constexpr int n2 = Cfg::n2;
@@ -382,7 +427,7 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
   }
 
   // ---- peaks -> candidates (cluster rank 0) ------------------------------------------
-  if (find_peaks && q == 0) {
+  if (mode != kPeaksNone && q == 0) {
     PView<C> Pv;
     Pv.n = n;
     if constexpr (C > 1) {
@@ -392,14 +437,15 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
     } else {
       Pv.base[0] = P;
     }
-    find_candidates<C, T>(p, Pv, t, status_in[t], w, ps);
+    if (mode == kPeaksMajor) find_major<C, T>(p, Pv, t, status_in[t], w.major, ps);
+    else find_candidates<C, T>(p, Pv, t, status_in[t], w, ps);
   }
   if constexpr (C > 1) cg::this_cluster().sync();  // keep our P alive while rank 0 reads it
 }
 
 template <int LOGN2, int C>
 static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
-                                 int find_peaks, cudaStream_t s) {
+                                 int mode, cudaStream_t s) {
   using Cfg = SpecCfg<LOGN2>;
   auto kern = spectrum_kernel<LOGN2, C>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::smem);
@@ -416,7 +462,7 @@ static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* s
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
-  e = cudaLaunchKernelEx(&cfg, kern, p, y, status_in, w, spectra, find_peaks);
+  e = cudaLaunchKernelEx(&cfg, kern, p, y, status_in, w, spectra, mode);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -547,7 +593,7 @@ constexpr size_t kDynSmem = (size_t)kBuf * sizeof(float2) + (size_t)kTw * sizeof
 template <int F>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     fused_spectrum_65536(Plan p, const float* __restrict__ x, Work w, float* __restrict__ y_out,
-                         float* __restrict__ spectra, int find_peaks, int nclusters) {
+                         float* __restrict__ spectra, int mode, int nclusters) {
   using namespace fz;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* buf = reinterpret_cast<float2*>(smem_raw);
@@ -617,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       if (sigma > 0.0) all_const = false;
     }
     // ---- a1 signal + DIF split into the two CTAs' buffers ------------------------------
-    float* yt = y_out + t * (int64_t)kN;
+    float* yt = y_out ? y_out + t * (int64_t)kN : nullptr;
 #pragma unroll 4
     for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
       const int j = q * (kn2 / 2) + jj;
@@ -635,8 +681,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       }
       const float2 za = make_float2(__double2float_rn(ya0), __double2float_rn(ya1));
       const float2 zb = make_float2(__double2float_rn(yb0), __double2float_rn(yb1));
-      reinterpret_cast<float2*>(yt)[j] = za;
-      reinterpret_cast<float2*>(yt + kn)[j] = zb;
+      if (y_out) {
+        reinterpret_cast<float2*>(yt)[j] = za;
+        reinterpret_cast<float2*>(yt + kn)[j] = zb;
+      }
       const float2 a0 = cadd(za, zb);
       float2 wj = twiddle(tw, j >> 1);  // W_32768^j = W_16384^(j/2) (x W_32768 if j odd)
       if (j & 1) wj = cmul(wj, w32768);
@@ -687,12 +735,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     // ---- a3 peaks -> candidates (rank 0) ------------------------------------------------
     if (q == 0) {
       const int32_t st = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
-      if (find_peaks) {
+      if (mode != kPeaksNone) {
         PView<2> Pv;
         Pv.n = kn;
         Pv.base[0] = P;
         Pv.base[1] = cluster.map_shared_rank(P, 1);
-        find_candidates<2, kT>(p, Pv, t, st, w, fs.ps);
+        if (mode == kPeaksMajor) find_major<2, kT>(p, Pv, t, st, w.major, fs.ps);
+        else find_candidates<2, kT>(p, Pv, t, st, w, fs.ps);
       } else if (threadIdx.x == 0) {
         w.status[t] = st;
       }
@@ -703,7 +752,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
 
 template <int F>
 static cudaError_t launch_fused_65536(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
-                                      bool find_peaks, cudaStream_t s) {
+                                      int mode, cudaStream_t s) {
   auto kern = fused_spectrum_65536<F>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::kDynSmem);
   if (e != cudaSuccess) return e;
@@ -719,27 +768,27 @@ static cudaError_t launch_fused_65536(const Plan& p, const float* x, Work w, flo
   }
   if ((int64_t)nclust > p.batch) nclust = (int)p.batch;
   cfg.gridDim = dim3(2 * nclust);
-  e = cudaLaunchKernelEx(&cfg, kern, p, x, w, y_out, spectra, find_peaks ? 1 : 0, nclust);
+  e = cudaLaunchKernelEx(&cfg, kern, p, x, w, y_out, spectra, mode, nclust);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
-                                  bool find_peaks, cudaStream_t s) {
+                                  int mode, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
   if (p.N != fz::kN) return cudaErrorInvalidValue;
   switch (p.F) {
-    case 1: return launch_fused_65536<1>(p, x, w, y_out, spectra, find_peaks, s);
-    case 2: return launch_fused_65536<2>(p, x, w, y_out, spectra, find_peaks, s);
-    case 3: return launch_fused_65536<3>(p, x, w, y_out, spectra, find_peaks, s);
+    case 1: return launch_fused_65536<1>(p, x, w, y_out, spectra, mode, s);
+    case 2: return launch_fused_65536<2>(p, x, w, y_out, spectra, mode, s);
+    case 3: return launch_fused_65536<3>(p, x, w, y_out, spectra, mode, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
-                            bool find_peaks, cudaStream_t s) {
+                            int mode, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
-  const int fp = find_peaks ? 1 : 0;
+  const int fp = mode;
   switch (p.log2N) {
     case 3: return launch_spec_t<2, 1>(p, y, status_in, w, spectra, fp, s);
     case 4: return launch_spec_t<3, 1>(p, y, status_in, w, spectra, fp, s);

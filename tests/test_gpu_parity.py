@@ -347,3 +347,69 @@ def test_similarity_stress_few_levels_and_outliers():
         if abs(got[q] - ref) > 1e-4 * max(ref, 1e-6):
             bad.append((int(ti[q]), int(pe[q]), got[q], ref))
     assert not bad
+
+
+# ---- spectral-only detector (oracle S1, reading R3) ------------------
+
+def _major_compare(x, spec, label):
+    p = g.params_for(spec)
+    res, _ = g.detect_major_periods(_to_dev(x), p)
+    torch.cuda.synchronize()
+    r = g.major_numpy(res)
+    ms = O.major_batch(x, O.params_for(spec, dft_band_only=spec.n_samples > 8192))
+    n_amb = 0
+    for i, m in enumerate(ms):
+        assert r[i]["status"] == m.status, (label, i)
+        if m.status != O.TRACE_OK:
+            assert r[i]["period"] == -1 and r[i]["bin"] == -1
+            continue
+        if m.ambiguous(1e-5):
+            n_amb += 1
+            continue
+        assert r[i]["bin"] == m.bin, (label, i, r[i]["bin"], m.bin, m.d_major)
+        assert r[i]["period"] == m.period
+        assert r[i]["period_s"] == np.float32(m.period_s)
+    assert n_amb <= max(1, len(ms) // 10), (label, n_amb)
+    return r
+
+
+@pytest.mark.parametrize("spec,n", [(tg.CFG1, 1), (tg.CFG2, 71), (tg.CFG3, 6), (tg.CFG5, 2)])
+def test_major_matches_oracle(spec, n):
+    x = tg.generate_host(spec.with_(batch=n))
+    _major_compare(x, spec, spec.name)
+
+
+@pytest.mark.parametrize("N,F", [(8, 1), (64, 2), (4096, 3), (65536, 1), (65536, 2), (131072, 3)])
+def test_major_shapes(N, F):
+    lo = 2 if N <= 8192 else N // 256  # keep the oracle's O(N * band) DFT short
+    spec = tg.CFG2.with_(batch=3, n_samples=N, n_features=F, min_period=lo, max_period=N // 2)
+    x = tg.generate_host(spec)
+    _major_compare(x, spec, f"N{N}F{F}")
+
+
+def test_major_equals_alg1_first_candidate():
+    # the first-ranked Alg. 1 candidate is f_major (same peaks, same order)
+    spec = tg.CFG3.with_(batch=64)
+    xd = torch.empty((64, spec.n_features * spec.n_samples), dtype=torch.float32, device="cuda")
+    tg.generate_device(spec, xd)
+    p = g.params_for(spec)
+    res, _ = g.detect_major_periods(xd, p)
+    _, det, _ = g.detect_periods(xd, p, detail=True)
+    torch.cuda.synchronize()
+    r, d = g.major_numpy(res), g.detail_numpy(det)
+    ok = r["status"] == 0
+    assert ok.sum() > 40
+    assert (r["bin"][ok] == d["cand_k"][ok, 0]).all()
+
+
+def test_major_statuses():
+    N = 1024
+    x = np.zeros((3, 1, N), np.float32)
+    x[1, 0] = np.arange(N)                          # monotone ramp: no in-band peak for [4, 16]
+    x[2, 0] = np.cos(2 * np.pi * 100 * np.arange(N) / N)  # period 10: in the band [4, 16]
+    spec = tg.CFG1.with_(batch=3, min_period=4, max_period=16)
+    p = g.params_for(spec)
+    res, _ = g.detect_major_periods(_to_dev(x), p)
+    r = g.major_numpy(res)
+    assert list(r["status"]) == [O.TRACE_CONSTANT, O.TRACE_APERIODIC, O.TRACE_OK]
+    assert r["bin"][2] == 100 and r["period"][2] == N // 100
