@@ -7,15 +7,16 @@
  * (paper_2201_01684_b200/) never links, imports or calls it, and shares no code,
  * header, table or constant generator with it.
  *
- * Everything is fp64 on the fp32 input bytes, sequential loops in the order the
- * paper writes them, one trace per call (callers parallelise over traces).
+ * Everything is fp64 on the fp32 input bytes (except the composite signal itself, formed
+ * in fp32 from fp64 statistics: reading Z23b), sequential loops in the order the paper
+ * writes them, one trace per call (callers parallelise over traces).
  * Compiled with -O2 -ffp-contract=off (no FMA contraction).
  *
  * Citations: P:n = /root/reference/PAPER.md line n. Readings Z1..Z30 are the ones
  * listed in SURVEY.md 8(c) and DESIGN.md "Readings".
  *
  * Steps:
- *   O1 composite detection signal              P:459 (+ Z1)
+ *   O1 composite detection signal              P:459 (+ Z1, Z23b)
  *   O2 power spectrum by the DFT definition     Alg.1 l.1-2, P:309-310 (+ Z2-Z4)
  *   O3 peaks -> candidate integer periods       Alg.1 l.3-5, P:311-314 (+ Z5-Z9, Z21)
  *   O4 Alg. 2 similarity error per candidate    P:353-382 (+ Z10-Z16)
@@ -88,14 +89,17 @@ typedef struct {
 /* ------------------------------------------------------------------------ */
 /* O1. Composite detection signal (P:459 names a composite of power, SM util and
  * mem util; Z1 reading: population z-score per channel, weighted sum, sigma=0
- * channel contributes 0, y rounded once to fp32):
- *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N),
- *   y[n] = fp32( sum_c a_c (x_c[n] - mu_c) ),  a_c = w_c / sigma_c  (Z23: the scale
- *   a_c is formed once per channel, products and sums in channel order, no FMA).
+ * channel contributes 0). Statistics in fp64 (two passes, Z23):
+ *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N);
+ * the centre and scale are rounded to fp32 once per channel (reading Z23b),
+ *   m_c = fp32(mu_c),  s_c = fp32(w_c / sigma_c),
+ * and the signal is formed in fp32, channel order, each operation rounded to nearest
+ * (no FMA):  y[n] = (...((0 + s_0 (x_0[n] - m_0)) + s_1 (x_1[n] - m_1)) + ...).
  * Returns 1 if every channel is constant. mu/sigma may be NULL. */
 int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, float* y, double* mu_out,
                      double* sigma_out) {
-  double mu[8], sigma[8], a[8];
+  double mu[8], sigma[8];
+  float m[8], sc[8];
   int all_const = 1;
   for (int c = 0; c < F; ++c) {
     const float* xc = x + (int64_t)c * N;
@@ -105,17 +109,22 @@ int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, floa
     double q = 0.0;
     for (int n = 0; n < N; ++n) q += ((double)xc[n] - mu[c]) * ((double)xc[n] - mu[c]);
     sigma[c] = sqrt(q / N);
-    a[c] = sigma[c] > 0.0 ? (w ? w[c] : 1.0) / sigma[c] : 0.0;
+    m[c] = (float)mu[c];
+    sc[c] = sigma[c] > 0.0 ? (float)((w ? w[c] : 1.0) / sigma[c]) : 0.0f;
     if (sigma[c] > 0.0) all_const = 0;
     if (mu_out) mu_out[c] = mu[c];
     if (sigma_out) sigma_out[c] = sigma[c];
   }
   for (int n = 0; n < N; ++n) {
-    double v = 0.0;
+    float v = 0.0f;
     for (int c = 0; c < F; ++c) {
-      if (sigma[c] > 0.0) v += a[c] * ((double)x[(int64_t)c * N + n] - mu[c]);
+      if (sigma[c] > 0.0) {
+        const float d = x[(int64_t)c * N + n] - m[c];
+        const float t = sc[c] * d;
+        v = v + t;
+      }
     }
-    y[n] = (float)v;
+    y[n] = v;
   }
   return all_const;
 }

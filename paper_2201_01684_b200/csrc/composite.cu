@@ -1,13 +1,14 @@
 // composite.cu — row a1: the composite detection signal (reading Z1/Z23).
 //
 //   mu_c = sum_n x_c[n] / N,   sigma_c^2 = sum_n (x_c[n] - x_c[0])^2 / N - (mu_c - x_c[0])^2
-//   y[n] = fp32( sum_c a_c (x_c[n] - mu_c) ),  a_c = w_c / sigma_c  (0 if sigma_c == 0)
+//   m_c = fp32(mu_c),  s_c = fp32(w_c / sigma_c)  (channels with sigma_c == 0 skipped)
+//   y[n] = fp32 channel-order sum of s_c (x_c[n] - m_c), each op rounded to nearest (Z23b)
 //
 // One CTA per trace, 512 threads. Pass 1 reads x once with 128-bit loads and forms the
 // fp64 sums (shifted by x_c[0] so the variance does not cancel); pass 2 re-reads x (an
-// L2 hit: the trace was just streamed) and writes y with 128-bit stores. fp64 with
-// explicit _rn intrinsics (no FMA) so y equals the oracle's rounding of the same
-// expression whenever mu and sigma agree to the last bit.
+// L2 hit: the trace was just streamed) and writes y with 128-bit stores. The fp32 ops use
+// explicit _rn intrinsics (no FMA), so y is bit-identical to the oracle's whenever m_c and
+// s_c round to the same fp32 values (the fp64 statistics agree to ~1e-16).
 #include "gpoeo_internal.cuh"
 
 namespace gpoeo {
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
   __shared__ double red[kCompThreads / 32];
   const int64_t t = blockIdx.x;
   const float* xt = x + t * stride;
-  double mu[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
+  float m[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
   bool all_const = true;
   for (int c = 0; c < F; ++c) {
     const float* xc = xt + (int64_t)c * N;
@@ -59,12 +60,13 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
     }
     s = block_sum(s, red);
     q = block_sum(q, red);
-    mu[c] = s / (double)N;
-    const double m = mu[c] - x0;
-    double var = q / (double)N - m * m;
+    const double mu = s / (double)N;
+    const double dm = mu - x0;
+    double var = q / (double)N - dm * dm;
     if (!(var > 0.0)) var = 0.0;
     const double sigma = sqrt(var);
-    a[c] = sigma > 0.0 ? (double)plan.w[c] / sigma : 0.0;
+    m[c] = __double2float_rn(mu);
+    a[c] = sigma > 0.0 ? __double2float_rn((double)plan.w[c] / sigma) : 0.f;
     if (sigma > 0.0) all_const = false;
   }
   if (threadIdx.x == 0) status[t] = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
@@ -72,25 +74,23 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
   if ((N & 3) == 0) {
 #pragma unroll 4
     for (int i = threadIdx.x; i < N / 4; i += kCompThreads) {
-      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
       for (int c = 0; c < F; ++c) {
-        if (a[c] == 0.0) continue;
+        if (a[c] == 0.f) continue;
         float4 xv = __ldg(reinterpret_cast<const float4*>(xt + (int64_t)c * N) + i);
-        v[0] = __dadd_rn(v[0], __dmul_rn(a[c], __dsub_rn((double)xv.x, mu[c])));
-        v[1] = __dadd_rn(v[1], __dmul_rn(a[c], __dsub_rn((double)xv.y, mu[c])));
-        v[2] = __dadd_rn(v[2], __dmul_rn(a[c], __dsub_rn((double)xv.z, mu[c])));
-        v[3] = __dadd_rn(v[3], __dmul_rn(a[c], __dsub_rn((double)xv.w, mu[c])));
+        v[0] = __fadd_rn(v[0], __fmul_rn(a[c], __fsub_rn(xv.x, m[c])));
+        v[1] = __fadd_rn(v[1], __fmul_rn(a[c], __fsub_rn(xv.y, m[c])));
+        v[2] = __fadd_rn(v[2], __fmul_rn(a[c], __fsub_rn(xv.z, m[c])));
+        v[3] = __fadd_rn(v[3], __fmul_rn(a[c], __fsub_rn(xv.w, m[c])));
       }
-      reinterpret_cast<float4*>(yt)[i] =
-          make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]), __double2float_rn(v[2]),
-                      __double2float_rn(v[3]));
+      reinterpret_cast<float4*>(yt)[i] = make_float4(v[0], v[1], v[2], v[3]);
     }
   } else {
     for (int i = threadIdx.x; i < N; i += kCompThreads) {
-      double v = 0.0;
+      float v = 0.f;
       for (int c = 0; c < F; ++c)
-        if (a[c] != 0.0) v = __dadd_rn(v, __dmul_rn(a[c], __dsub_rn((double)__ldg(xt + (int64_t)c * N + i), mu[c])));
-      yt[i] = __double2float_rn(v);
+        if (a[c] != 0.f) v = __fadd_rn(v, __fmul_rn(a[c], __fsub_rn(__ldg(xt + (int64_t)c * N + i), m[c])));
+      yt[i] = v;
     }
   }
 }

@@ -156,39 +156,19 @@ struct PView {
   }
 };
 
-// Rows a3: in-band peaks -> top-K (P desc, k asc) -> c_peak threshold -> L = floor(N/k) ->
-// dedupe (Alg.1 l.3-5; Z5, Z7-Z9); appends one Alg. 2 query per candidate and
-// writes the trace status. Called by the whole CTA (T threads) of cluster rank 0.
+// Rows a3, second half: given the in-band peak maximum pmax (< 0: no peak) and the peaks
+// above c_peak^2 pmax collected in ps (ps.count of them, the first kPeakCap stored), keep
+// the top K by (P desc, k asc), map k -> floor(N/k) and dedupe (Alg.1 l.3-5, P:311-314;
+// Z5, Z7-Z9); append one Alg. 2 query per candidate and write the trace status. Called
+// by the whole CTA (T threads) that owns ps; Pv sees the whole spectrum.
 template <int C, int T>
-__device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps) {
+__device__ void finish_candidates(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps,
+                                  float pmax) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = T / 32;
-  // pass 1: P_max over in-band peaks
-  float best = -1.f;
-  for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
-    const float pk = Pv(k);
-    if (pk > Pv(k - 1) && pk >= Pv(k + 1)) best = fmaxf(best, pk);
-  }
-  for (int off = 16; off; off >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
-  if (lane == 0) ps.redP[warp] = best;
-  if (threadIdx.x == 0) { ps.count = 0; ps.overflow = 0; }
-  __syncthreads();
-  float pmax = -1.f;
-  for (int i = 0; i < NW; ++i) pmax = fmaxf(pmax, ps.redP[i]);
   const double thr = (double)p.c_peak * (double)p.c_peak * (double)pmax;
   int nc = 0;
   if (pmax >= 0.f) {
-    // pass 2: peaks above the threshold
-    for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
-      const float pk = Pv(k);
-      if (pk > Pv(k - 1) && pk >= Pv(k + 1) && (double)pk > thr) {
-        const int slot = atomicAdd(&ps.count, 1);
-        if (slot < kPeakCap) {
-          ps.pk_P[slot] = pk;
-          ps.pk_k[slot] = (int32_t)k;
-        }
-      }
-    }
     __syncthreads();
     const int cnt = ps.count;
     if (cnt <= kPeakCap) {
@@ -280,7 +260,39 @@ __device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, in
       for (int c2 = 0; c2 < nc; ++c2) append_item(w.list_a, (int)t, w.cand_L[t * p.K + c2], (int)(t * p.K + c2));
     }
   }
+}
 
+// Rows a3 on one CTA: P_max over the in-band peaks, collect the peaks above the
+// threshold, then finish_candidates. Called by the whole CTA of cluster rank 0.
+template <int C, int T>
+__device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = T / 32;
+  float best = -1.f;
+  for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
+    const float pk = Pv(k);
+    if (pk > Pv(k - 1) && pk >= Pv(k + 1)) best = fmaxf(best, pk);
+  }
+  for (int off = 16; off; off >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, off));
+  if (lane == 0) ps.redP[warp] = best;
+  if (threadIdx.x == 0) { ps.count = 0; ps.overflow = 0; }
+  __syncthreads();
+  float pmax = -1.f;
+  for (int i = 0; i < NW; ++i) pmax = fmaxf(pmax, ps.redP[i]);
+  const double thr = (double)p.c_peak * (double)p.c_peak * (double)pmax;
+  if (pmax >= 0.f) {
+    for (int64_t k = p.k_lo + threadIdx.x; k <= p.k_hi; k += T) {
+      const float pk = Pv(k);
+      if (pk > Pv(k - 1) && pk >= Pv(k + 1) && (double)pk > thr) {
+        const int slot = atomicAdd(&ps.count, 1);
+        if (slot < kPeakCap) {
+          ps.pk_P[slot] = pk;
+          ps.pk_k[slot] = (int32_t)k;
+        }
+      }
+    }
+  }
+  finish_candidates<C, T>(p, Pv, t, st, w, ps, pmax);
 }
 
 // Spectral-only detector (reading R3): the in-band peak with the largest P, ties
@@ -467,24 +479,10 @@ static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* s
   return cudaGetLastError();
 }
 
-// ===================================================================================
-// Fused rows a1 + a2 + a3 for N = 65536 (BASELINE configs 3 and 4): the composite, the
-// FFT power spectrum and the peak picking in ONE persistent kernel per 2-CTA cluster, so
-// the trace x[F][N] is read from HBM once (the stats pass and the signal pass touch the
-// same two quarter-blocks per CTA; the second read is an L2 hit) and y is written once
-// (for the Alg. 2 scorer). Same arithmetic as composite_kernel + spectrum_kernel<14, 2>:
-//   stats: fp64 sums, shifted by x_c[0]; CTA partials added in rank order;
-//   y = fp32(sum_c a_c (x_c - mu_c)) with _rn intrinsics;
-//   DIF split a_0[j] = z[j] + z[j + n2], a_1[j] = (z[j] - z[j + n2]) W_n^j built while y
-//   is formed (CTA q owns j in [q n2/2, (q+1) n2/2) and stores the other half into its
-//   partner's shared memory through DSMEM);
-//   n2 = 16384-point FFT: three in-place Stockham passes (radix 32, 32, 16) with the
-//   butterflies in registers, twiddles from a quarter-wave table in shared memory, one
-//   pad slot per 32 entries (conflict-free strided writes).
 namespace fz {
 constexpr int kN = 65536, kn = 32768, kn2 = 16384, kT = 512;
-constexpr int kBuf = kn2 + kn2 / 32;  // padded float2 entries
-constexpr int kTw = kn2 / 4;          // quarter-wave table W_16384^m, m < 4096
+constexpr int kBuf = kn2 + kn2 / 32;  // padded float2 entries (>= kn + 1 floats: the full P fits)
+constexpr int kTw = kn2 / 2;          // half-wave table W_16384^m, m < 8192
 __device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
 
 __constant__ float2 kW32[22] = {
@@ -499,15 +497,11 @@ __constant__ float2 kW32[22] = {
 
 __constant__ float2 kW65536[4] = {{1.000000000e+00f, -0.000000000e+00f}, {9.999999954e-01f, -9.587379910e-05f}, {9.999999816e-01f, -1.917475973e-04f}, {9.999999586e-01f, -2.876213938e-04f}};
 
-// W_16384^m from the quarter table: W^m = (-i)^(m >> 12) * tw[m & 4095]
+// W_16384^m (0 <= m < 16384) from the half-wave table: W^m = -W^(m - 8192) for m >= 8192
 __device__ __forceinline__ float2 twiddle(const float2* tw, int m) {
   const float2 b = tw[m & (kTw - 1)];
-  switch ((m >> 12) & 3) {
-    case 0: return b;
-    case 1: return make_float2(b.y, -b.x);
-    case 2: return make_float2(-b.x, -b.y);
-    default: return make_float2(-b.y, b.x);
-  }
+  const unsigned s = ((unsigned)m << 18) & 0x80000000u;  // bit 13 -> sign
+  return make_float2(__uint_as_float(__float_as_uint(b.x) ^ s), __uint_as_float(__float_as_uint(b.y) ^ s));
 }
 
 // In-place 32-point DFT: n = 8 n1 + n2, k = k1 + 4 k2: DFT4 over n1 (elements n2 + 8 n1),
@@ -540,6 +534,8 @@ __device__ __forceinline__ void dft16(float2* v) {
 }
 __device__ __forceinline__ constexpr int out16(int r) { return (r >> 2) + 4 * (r & 3); }
 
+// One in-place Stockham pass. Twiddles w^r, w = W^step: every 8th power from the table,
+// the others by at most 7 successive products (error well inside the 1e-4 bar, Z29).
 template <int R>
 __device__ __forceinline__ void pass(float2* buf, const float2* tw, int Ns) {
   constexpr int NB = kn2 / R;
@@ -558,8 +554,13 @@ __device__ __forceinline__ void pass(float2* buf, const float2* tw, int Ns) {
     const int k = j & (Ns - 1);
     if (Ns > 1) {
       const int step = k * (kn2 / (Ns * R));
+      const float2 w1 = twiddle(tw, step);
+      float2 wr = w1;
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], twiddle(tw, step * r));
+      for (int r = 1; r < R; ++r) {
+        if (r > 1) wr = (r % 8 == 0) ? twiddle(tw, step * r) : cmul(wr, w1);
+        v[b][r] = cmul(v[b][r], wr);
+      }
     }
     if constexpr (R == 32) dft32(v[b]);
     else dft16(v[b]);
@@ -586,10 +587,54 @@ struct FusedShared {
   PeakShared ps;
   double red[kT / 32];
   double stat[2][GPOEO_MAX_FEATURES][2];  // [rank][channel][sum, shifted sum of squares]
+  float pm[2];                            // per-rank in-band peak maximum
+  int32_t pk[2];                          // per-rank bin of that maximum (major mode)
 };
 constexpr size_t kDynSmem = (size_t)kBuf * sizeof(float2) + (size_t)kTw * sizeof(float2);
+
+// P[k] of the full spectrum held contiguously in shared memory, mirrored edges (Z5)
+__device__ __forceinline__ float pget(const float* P, int k) {
+  if (k < 0) k = -k;
+  if (k > kn) k = 2 * kn - k;
+  return P[k];
+}
+__device__ __forceinline__ bool is_peak(const float* P, int k) {
+  const float pk = P[k];
+  return pk > pget(P, k - 1) && pk >= pget(P, k + 1);
+}
+
+// L2 prefetch of this CTA's half of trace t (quarter blocks q and 2 + q of every channel):
+// streamed while the CTA runs the FFT of the previous trace.
+template <int F>
+__device__ __forceinline__ void prefetch_half(const float* xt, int q) {
+  constexpr int kChunk = 16384;                   // bytes per bulk prefetch
+  constexpr int kPer = (kn2 / 2) * 4 * 2 / kChunk;  // chunks per channel (two 64 KB blocks)
+  const int i = threadIdx.x;
+  if (i < F * kPer) {
+    const int c = i / kPer, u = i % kPer;
+    const int blk = (u < kPer / 2) ? q : 2 + q;
+    const char* a = reinterpret_cast<const char*>(xt + (int64_t)c * kN + (int64_t)blk * (kn2 / 2) * 2) +
+                    (size_t)(u % (kPer / 2)) * kChunk;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(kChunk) : "memory");
+  }
+}
 }  // namespace fz
 
+// ===================================================================================
+// Fused rows a1 + a2 + a3 for N = 65536 (BASELINE configs 3 and 4), one persistent kernel
+// per 2-CTA cluster, one trace at a time per cluster:
+//   A  stats: CTA q reads quarter blocks {q, 2+q} of every channel once (HBM, or L2 when
+//      prefetched), fp64 sums shifted by x_c[0]; partials exchanged through DSMEM.
+//   B  signal: re-reads the same blocks (L2), y = fp32 channel sum of s_c (x_c - m_c) (Z23b),
+//      writes y once when the scorer needs it (never in spectral-only mode), and builds
+//      the DIF halves a_0[j] = z[j] + z[j + n2], a_1[j] = (z[j] - z[j + n2]) W^j straight
+//      into the two CTAs' shared memory; then prefetches its half of the next trace to L2.
+//   C  16384-point in-place Stockham FFT per CTA (radix 32, 32, 16; butterflies in
+//      registers; half-wave twiddle table in shared memory; one pad slot per 32 entries).
+//   D  R2C post: P[2 k2 + q]; every CTA then holds the FULL spectrum P[0..n] contiguously
+//      (each writes its bins into both CTAs' buffers).
+//   E  peaks: each CTA scans half of the band; Alg. 1 candidates (mode 1) or f_major (mode 2)
+//      combined on rank 0 through DSMEM.
 template <int F>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     fused_spectrum_65536(Plan p, const float* __restrict__ x, Work w, float* __restrict__ y_out,
@@ -603,24 +648,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
   const int q = (int)cluster.block_rank();
   const int cid = blockIdx.x / 2;
   float2* pbuf = cluster.map_shared_rank(buf, q ^ 1);
+  FusedShared* pfs = cluster.map_shared_rank(&fs, q ^ 1);
+  FusedShared* fs0 = cluster.map_shared_rank(&fs, 0);
   for (int m = threadIdx.x; m < kTw; m += kT) {
     float s, c;
     sincospif(-2.0f * (float)m / (float)kn2, &s, &c);
     tw[m] = make_float2(c, s);
   }
   const float2 w32768 = make_float2(9.999999816164e-01f, -1.917475973107e-04f);
+  if (cid < p.batch) prefetch_half<F>(x + (int64_t)cid * p.stride, q);
   for (int64_t t = cid; t < p.batch; t += nclusters) {
     const float* xt = x + t * p.stride;
-    // ---- a1 stats over my quarter blocks {q, 2 + q} ----------------------------------
-    double mu[F], a[F];
+    // ---- A: stats over my quarter blocks {q, 2 + q} -----------------------------------
 #pragma unroll
     for (int c = 0; c < F; ++c) {
       const float* xc = xt + (int64_t)c * kN;
       const double x0 = (double)__ldg(xc);
       double s = 0.0, qq = 0.0;
       const float4* x4 = reinterpret_cast<const float4*>(xc);
-      // 16 float4 per thread: issue them all before the fp64 math (bytes in flight:
-      // 512 threads x 256 B per SM, enough to cover HBM latency)
       float4 buf4[kn2 / 2 / kT];
 #pragma unroll
       for (int u = 0; u < kn2 / 2 / kT; ++u) {
@@ -641,47 +686,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       if (threadIdx.x == 0) {
         fs.stat[q][c][0] = s;
         fs.stat[q][c][1] = qq;
-        FusedShared* pfs = cluster.map_shared_rank(&fs, q ^ 1);
         pfs->stat[q][c][0] = s;
         pfs->stat[q][c][1] = qq;
       }
-      (void)x0;
     }
     cluster.sync();
     bool all_const = true;
+    float m[F], a[F];
 #pragma unroll
     for (int c = 0; c < F; ++c) {
       const double x0 = (double)__ldg(xt + (int64_t)c * kN);
       const double s = fs.stat[0][c][0] + fs.stat[1][c][0];
       const double qq = fs.stat[0][c][1] + fs.stat[1][c][1];
-      mu[c] = s / (double)kN;
-      const double m = mu[c] - x0;
-      double var = qq / (double)kN - m * m;
+      const double mu = s / (double)kN;
+      const double dm = mu - x0;
+      double var = qq / (double)kN - dm * dm;
       if (!(var > 0.0)) var = 0.0;
       const double sigma = sqrt(var);
-      a[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
+      m[c] = __double2float_rn(mu);
+      a[c] = sigma > 0.0 ? __double2float_rn((double)p.w[c] / sigma) : 0.f;
       if (sigma > 0.0) all_const = false;
     }
-    // ---- a1 signal + DIF split into the two CTAs' buffers ------------------------------
+    // ---- B: signal + DIF split into the two CTAs' buffers ------------------------------
     float* yt = y_out ? y_out + t * (int64_t)kN : nullptr;
 #pragma unroll 4
     for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
       const int j = q * (kn2 / 2) + jj;
-      double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+      float ya0 = 0.f, ya1 = 0.f, yb0 = 0.f, yb1 = 0.f;
 #pragma unroll
       for (int c = 0; c < F; ++c) {
-        if (a[c] == 0.0) continue;
+        if (a[c] == 0.f) continue;
         const float* xc = xt + (int64_t)c * kN;
         const float2 xa = __ldg(reinterpret_cast<const float2*>(xc + 2 * j));
         const float2 xb = __ldg(reinterpret_cast<const float2*>(xc + 2 * j + kn));
-        ya0 = __dadd_rn(ya0, __dmul_rn(a[c], __dsub_rn((double)xa.x, mu[c])));
-        ya1 = __dadd_rn(ya1, __dmul_rn(a[c], __dsub_rn((double)xa.y, mu[c])));
-        yb0 = __dadd_rn(yb0, __dmul_rn(a[c], __dsub_rn((double)xb.x, mu[c])));
-        yb1 = __dadd_rn(yb1, __dmul_rn(a[c], __dsub_rn((double)xb.y, mu[c])));
+        ya0 = __fadd_rn(ya0, __fmul_rn(a[c], __fsub_rn(xa.x, m[c])));
+        ya1 = __fadd_rn(ya1, __fmul_rn(a[c], __fsub_rn(xa.y, m[c])));
+        yb0 = __fadd_rn(yb0, __fmul_rn(a[c], __fsub_rn(xb.x, m[c])));
+        yb1 = __fadd_rn(yb1, __fmul_rn(a[c], __fsub_rn(xb.y, m[c])));
       }
-      const float2 za = make_float2(__double2float_rn(ya0), __double2float_rn(ya1));
-      const float2 zb = make_float2(__double2float_rn(yb0), __double2float_rn(yb1));
-      if (y_out) {
+      const float2 za = make_float2(ya0, ya1);
+      const float2 zb = make_float2(yb0, yb1);
+      if (yt) {
         reinterpret_cast<float2*>(yt)[j] = za;
         reinterpret_cast<float2*>(yt + kn)[j] = zb;
       }
@@ -692,12 +737,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       buf[pad(j)] = q == 0 ? a0 : a1;
       pbuf[pad(j)] = q == 0 ? a1 : a0;
     }
+    // this trace's x is consumed: stream my half of the next one into L2 during C-E
+    if (t + nclusters < p.batch) prefetch_half<F>(x + (t + nclusters) * p.stride, q);
     cluster.sync();
-    // ---- a2 FFT (16384 points per CTA) -----------------------------------------------
+    // ---- C: FFT (16384 points per CTA) -----------------------------------------------
     pass<32>(buf, tw, 1);
     pass<32>(buf, tw, 32);
     pass<16>(buf, tw, 1024);
-    // ---- R2C post: P[2 k2 + q] (C = 2: partner bins sit in the same CTA) ---------------
+    // ---- D: R2C post: P[2 k2 + q] (C = 2: partner bins sit in the same CTA) ------------
     constexpr int PER = kn2 / kT;
     float pv[PER];
 #pragma unroll
@@ -719,8 +766,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       const float xr = Z0.x - Z0.y;
       pnyq = xr * xr;
     }
-    __syncthreads();
+    __syncthreads();  // my Z fully read (C = 2: the R2C partner bins are local)
+    // my bins in place: P_loc[k2] = P[2 k2 + q]; the neighbours of my bins are the
+    // partner's (DSMEM reads in phase E)
     float* P = reinterpret_cast<float*>(buf);
+    const float* Pp = reinterpret_cast<const float*>(pbuf);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int k2 = threadIdx.x + i * kT;
@@ -731,23 +781,90 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       P[kn2] = pnyq;
       if (spectra) spectra[t * (int64_t)(kn + 1) + kn] = pnyq;
     }
+    if (mode == kPeaksCandidates && q == 0 && threadIdx.x == 0) fs.ps.count = 0;
     cluster.sync();
-    // ---- a3 peaks -> candidates (rank 0) ------------------------------------------------
-    if (q == 0) {
-      const int32_t st = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
-      if (mode != kPeaksNone) {
-        PView<2> Pv;
-        Pv.n = kn;
-        Pv.base[0] = P;
-        Pv.base[1] = cluster.map_shared_rank(P, 1);
-        if (mode == kPeaksMajor) find_major<2, kT>(p, Pv, t, st, w.major, fs.ps);
-        else find_candidates<2, kT>(p, Pv, t, st, w, fs.ps);
-      } else if (threadIdx.x == 0) {
-        w.status[t] = st;
+    // ---- E: peaks over my bins k = 2 k2 + q of the band ----------------------------------
+    const int32_t st = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k2lo = (p.k_lo - q + 1) >> 1, k2hi = (p.k_hi - q) >> 1;  // 2 k2 + q in [k_lo, k_hi]
+    // Z5 with mirrored edges: P[k-1], P[k+1] live in the partner (k = n: P[n+1] = P[n-1])
+    auto peak_at = [&](int k2) -> bool {
+      const float pk = P[k2];
+      const float left = Pp[k2 - 1 + q];
+      const float right = (q == 0 && k2 == kn2) ? Pp[kn2 - 1] : Pp[k2 + q];
+      return pk > left && pk >= right;
+    };
+    if (mode == kPeaksNone) {
+      if (q == 0 && threadIdx.x == 0) w.status[t] = st;
+    } else {
+      // the largest of my peaks (k increases with k2: strict > keeps the smaller k)
+      float bp = -1.f;
+      int32_t bk = 0x7fffffff;
+      for (int k2 = k2lo + threadIdx.x; k2 <= k2hi; k2 += kT)
+        if (P[k2] > bp && peak_at(k2)) { bp = P[k2]; bk = 2 * k2 + q; }
+      for (int off = 16; off; off >>= 1) {
+        const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+        const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+        if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+      }
+      if (lane == 0) { fs.ps.redP[warp] = bp; fs.ps.redk[warp] = bk; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int i = 1; i < kT / 32; ++i) {
+          const float op = fs.ps.redP[i];
+          const int32_t ok = fs.ps.redk[i];
+          if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+        }
+        fs.pm[q] = bp;
+        fs.pk[q] = bk;
+        pfs->pm[q] = bp;
+        pfs->pk[q] = bk;
+      }
+      cluster.sync();
+      float pmax = fs.pm[0];
+      int32_t kmax = fs.pk[0];
+      if (fs.pm[1] > pmax || (fs.pm[1] == pmax && fs.pk[1] < kmax)) { pmax = fs.pm[1]; kmax = fs.pk[1]; }
+      if (mode == kPeaksMajor) {
+        if (q == 0 && threadIdx.x == 0) {
+          int32_t status = st;
+          if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;
+          if (status == GPOEO_TRACE_OK && pmax < 0.f) status = GPOEO_TRACE_APERIODIC;
+          gpoeo_major_result r;
+          r.status = status;
+          r.bin = status == GPOEO_TRACE_OK ? kmax : -1;
+          r.period = status == GPOEO_TRACE_OK ? p.N / kmax : -1;
+          r.period_s = status == GPOEO_TRACE_OK ? (float)((double)r.period * p.Ts) : -1.f;
+          w.major[t] = r;
+        }
+      } else {
+        // Alg. 1 l.3-5: peaks above c^2 P_max, collected on rank 0 (Z3, Z5, Z7)
+        const double thr = (double)p.c_peak * (double)p.c_peak * (double)pmax;
+        if (pmax >= 0.f) {
+          for (int k2 = k2lo + threadIdx.x; k2 <= k2hi; k2 += kT) {
+            const float pk = P[k2];
+            if ((double)pk > thr && peak_at(k2)) {
+              const int slot = atomicAdd(&fs0->ps.count, 1);
+              if (slot < kPeakCap) {
+                fs0->ps.pk_P[slot] = pk;
+                fs0->ps.pk_k[slot] = 2 * k2 + q;
+              }
+            }
+          }
+        }
+        cluster.sync();
+        if (q == 0) {
+          PView<2> Pv;
+          Pv.n = kn;
+          Pv.base[0] = P;
+          Pv.base[1] = Pp;
+          finish_candidates<2, kT>(p, Pv, t, st, w, fs.ps, pmax);
+        }
       }
     }
-    cluster.sync();  // partner P read; buffers free for the next trace
+    // no end-of-trace barrier: the next trace's first cluster.sync (after its stats, which
+    // touch neither buffer) orders my buffer writes after the partner's phase-E reads
   }
+  cluster.sync();  // the partner may still read my shared memory: do not exit before it is done
 }
 
 template <int F>
