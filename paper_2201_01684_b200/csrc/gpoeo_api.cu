@@ -92,7 +92,7 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
 
 struct Layout {
   size_t off_y, off_status, off_ncand, off_ck, off_cL, off_cP, off_cerr, off_bb, off_llo, off_lhi, off_lbase,
-      off_ia, off_ib, off_lerr, off_lab, off_ctr, total;
+      off_ia, off_ib, off_xa, off_xb, off_lerr, off_lab, off_ctr, total;
   int32_t lab_stride;
 };
 
@@ -119,6 +119,10 @@ Layout layout(const Plan& pl) {
   L.off_lbase = take(sizeof(int64_t) * B);
   L.off_ia = take(sizeof(int4) * B * K);
   L.off_ib = take(sizeof(int4) * B * ML);
+  // xl arrays (L > kBucketSplitL) only when the band reaches there
+  const bool xl = pl.Lmax > kBucketSplitL;
+  L.off_xa = take(xl ? sizeof(int4) * B * K : 0);
+  L.off_xb = take(xl ? sizeof(int4) * B * ML : 0);
   L.off_lerr = take(sizeof(double) * B * ML);
   L.lab_stride = pl.Lmax > kLabCap ? ((pl.Lmax + 15) & ~15) : 0;  // streaming path (L > 8192)
   L.off_lab = take((size_t)kMaxScoreCtas * (kScoreThreads / 32) * (size_t)L.lab_stride);
@@ -142,9 +146,11 @@ Work carve(const Plan& pl, const Layout& L, void* ws) {
   w.local_hi = reinterpret_cast<int32_t*>(b + L.off_lhi);
   w.local_base = reinterpret_cast<int64_t*>(b + L.off_lbase);
   w.list_a = ItemList{reinterpret_cast<int4*>(b + L.off_ia), (int64_t)pl.batch * pl.K, &w.ctr[CTR_A_SMALL],
-                      &w.ctr[CTR_A_BIG], &w.ctr[CTR_CUR_A_SMALL], &w.ctr[CTR_CUR_A_BIG]};
+                      &w.ctr[CTR_A_BIG], &w.ctr[CTR_CUR_A_SMALL], &w.ctr[CTR_CUR_A_BIG],
+                      reinterpret_cast<int4*>(b + L.off_xa), &w.ctr[CTR_A_XL], &w.ctr[CTR_CUR_A_XL]};
   w.list_b = ItemList{reinterpret_cast<int4*>(b + L.off_ib), (int64_t)pl.batch * pl.max_local, &w.ctr[CTR_B_SMALL],
-                      &w.ctr[CTR_B_BIG], &w.ctr[CTR_CUR_B_SMALL], &w.ctr[CTR_CUR_B_BIG]};
+                      &w.ctr[CTR_B_BIG], &w.ctr[CTR_CUR_B_SMALL], &w.ctr[CTR_CUR_B_BIG],
+                      reinterpret_cast<int4*>(b + L.off_xb), &w.ctr[CTR_B_XL], &w.ctr[CTR_CUR_B_XL]};
   w.local_err = reinterpret_cast<double*>(b + L.off_lerr);
   w.lab_scratch = L.lab_stride ? reinterpret_cast<uint8_t*>(b + L.off_lab) : nullptr;
   w.major = nullptr;
@@ -411,7 +417,7 @@ int gpoeo_detect_major_periods(const float* traces, int64_t batch, const gpoeo_p
 size_t gpoeo_similarity_workspace_size(int64_t n_queries) {
   if (n_queries < 0) return 0;
   size_t o = align_up(sizeof(unsigned long long) * kCounterSlots);
-  o += align_up(sizeof(int4) * (size_t)(n_queries > 0 ? n_queries : 1));
+  o += 2 * align_up(sizeof(int4) * (size_t)(n_queries > 0 ? n_queries : 1));  // items + xl
   // label scratch sized for the largest supported L (only used when L > kLabCap)
   o += align_up((size_t)kMaxScoreCtas * (kScoreThreads / 32) * (size_t)((1 << GPOEO_MAX_LOG2N) / 2));
   return o;
@@ -434,15 +440,18 @@ int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples
   char* b = static_cast<char*>(workspace);
   unsigned long long* ctr = reinterpret_cast<unsigned long long*>(b);
   int4* items = reinterpret_cast<int4*>(b + align_up(sizeof(unsigned long long) * kCounterSlots));
+  int4* xl = reinterpret_cast<int4*>(b + align_up(sizeof(unsigned long long) * kCounterSlots) +
+                                     align_up(sizeof(int4) * (size_t)n_queries));
   uint8_t* lab = reinterpret_cast<uint8_t*>(b + align_up(sizeof(unsigned long long) * kCounterSlots) +
-                                            align_up(sizeof(int4) * (size_t)n_queries));
+                                            2 * align_up(sizeof(int4) * (size_t)n_queries));
   Plan pl;
   memset(&pl, 0, sizeof(pl));
   pl.N = n_samples;
   pl.G = num_groups;
   pl.maxit = gmm_max_iters;
   pl.batch = batch;
-  ItemList list{items, n_queries, &ctr[CTR_A_SMALL], &ctr[CTR_A_BIG], &ctr[CTR_CUR_A_SMALL], &ctr[CTR_CUR_A_BIG]};
+  ItemList list{items, n_queries, &ctr[CTR_A_SMALL], &ctr[CTR_A_BIG], &ctr[CTR_CUR_A_SMALL], &ctr[CTR_CUR_A_BIG],
+                xl, &ctr[CTR_A_XL], &ctr[CTR_CUR_A_XL]};
   CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
   pack_items_kernel<<<(unsigned)((n_queries + 255) / 256), 256, 0, s>>>(trace_index, period, n_queries, list);
   CK(cudaGetLastError());
@@ -460,8 +469,8 @@ int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t ba
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaMemcpyAsync(h, workspace, sizeof(h), cudaMemcpyDeviceToHost, s) != cudaSuccess) return GPOEO_ERR_CUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return GPOEO_ERR_CUDA;
-  out->n_candidate_queries = (int64_t)(h[CTR_A_SMALL] + h[CTR_A_BIG]);
-  out->n_local_queries = (int64_t)(h[CTR_B_SMALL] + h[CTR_B_BIG]);
+  out->n_candidate_queries = (int64_t)(h[CTR_A_SMALL] + h[CTR_A_BIG] + h[CTR_A_XL]);
+  out->n_local_queries = (int64_t)(h[CTR_B_SMALL] + h[CTR_B_BIG] + h[CTR_B_XL]);
   out->cem_sample_passes = (int64_t)h[CTR_CEM_PASSES];
   return GPOEO_OK;
 }

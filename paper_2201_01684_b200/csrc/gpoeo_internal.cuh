@@ -41,15 +41,25 @@ enum CounterSlot {
   CTR_CUR_B_BIG = 7,
   CTR_CEM_PASSES = 8,  // sum of CEM sample passes (work counter)
   CTR_LOCAL_SLOTS = 9, // local-score slots handed out by select
+  CTR_A_XL = 10,       // candidate queries with L > kBucketSplitL (the xl array)
+  CTR_B_XL = 11,       // local queries with L > kBucketSplitL
+  CTR_CUR_A_XL = 12,
+  CTR_CUR_B_XL = 13,
 };
 
 #ifndef GPOEO_BUCKET_MIN_L
 #define GPOEO_BUCKET_MIN_L 513
 #endif
 constexpr int kBucketMinL = GPOEO_BUCKET_MIN_L;  // L >= this: bucketed warp path (score.cu)
+#ifndef GPOEO_BUCKET_SPLIT_L
+#define GPOEO_BUCKET_SPLIT_L 2048
+#endif
+constexpr int kBucketSplitL = GPOEO_BUCKET_SPLIT_L;  // L > this: the xl list (larger shared-memory regions)
 
-// A query list: small-L items packed from the front, the others from the back, so the
-// two scorer kernels (team path / bucketed path) each read one contiguous range.
+// A query list: small-L items packed from the front of `items`, mid-L items from its back,
+// so the team kernel and the bucketed kernel each read one contiguous range; L above
+// kBucketSplitL go to `xl` (scored by a bucketed launch with larger regions, so the common
+// mid range runs at higher occupancy).
 struct ItemList {
   int4* items;
   int64_t cap;
@@ -57,27 +67,38 @@ struct ItemList {
   unsigned long long* n_big;
   unsigned long long* cur_small;
   unsigned long long* cur_big;
+  int4* xl;  // [cap]
+  unsigned long long* n_xl;
+  unsigned long long* cur_xl;
 };
 
 __device__ __forceinline__ void append_items(const ItemList& l, int t, int L0, int count, int slot0) {
   // items (t, L0 + i, slot0 + i), i < count; L increasing
   int ns = 0;
   while (ns < count && L0 + ns < kBucketMinL) ++ns;
+  int nm = ns;
+  while (nm < count && L0 + nm <= kBucketSplitL) ++nm;
   if (ns) {
     const unsigned long long b = atomicAdd(l.n_small, (unsigned long long)ns);
     for (int i = 0; i < ns; ++i) l.items[b + i] = make_int4(t, L0 + i, slot0 + i, 0);
   }
-  if (count - ns) {
-    const unsigned long long b = atomicAdd(l.n_big, (unsigned long long)(count - ns));
-    for (int i = ns; i < count; ++i) l.items[l.cap - 1 - (int64_t)(b + (i - ns))] = make_int4(t, L0 + i, slot0 + i, 0);
+  if (nm - ns) {
+    const unsigned long long b = atomicAdd(l.n_big, (unsigned long long)(nm - ns));
+    for (int i = ns; i < nm; ++i) l.items[l.cap - 1 - (int64_t)(b + (i - ns))] = make_int4(t, L0 + i, slot0 + i, 0);
+  }
+  if (count - nm) {
+    const unsigned long long b = atomicAdd(l.n_xl, (unsigned long long)(count - nm));
+    for (int i = nm; i < count; ++i) l.xl[b + (i - nm)] = make_int4(t, L0 + i, slot0 + i, 0);
   }
 }
 
 __device__ __forceinline__ void append_item(const ItemList& l, int t, int L, int slot) {
   if (L < kBucketMinL) {
     l.items[atomicAdd(l.n_small, 1ull)] = make_int4(t, L, slot, 0);
-  } else {
+  } else if (L <= kBucketSplitL) {
     l.items[l.cap - 1 - (int64_t)atomicAdd(l.n_big, 1ull)] = make_int4(t, L, slot, 0);
+  } else {
+    l.xl[atomicAdd(l.n_xl, 1ull)] = make_int4(t, L, slot, 0);
   }
 }
 

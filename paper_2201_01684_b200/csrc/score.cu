@@ -26,6 +26,8 @@
 //  * L > 16*256: a warp owns the pair and streams samples from L1/L2 every pass (labels in
 //    shared memory or global scratch).
 //  * Err(L) is the sum of per-team partial sums in team order: deterministic.
+#include <stdlib.h>
+
 #include "gpoeo_internal.cuh"
 
 namespace gpoeo {
@@ -39,10 +41,18 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifdef GPOEO_STATS
 // debug build only: [0] bucket pairs, [1] bucket passes, [2] members swept (straddling +
 // relabelled), [3] straddling members, [4] straddling buckets, [5] team pairs, [6] team passes
-__device__ unsigned long long g_stats[8];
+__device__ unsigned long long g_stats[16];
 #define GPOEO_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+// [8..11]: bucket-path cycles of lane 0 in (range + counting sort), bucket sums, CEM passes, final
+#define GPOEO_TICK(i, t0)                                  \
+  do {                                                     \
+    const long long t1_ = clock64();                       \
+    if (lane == 0) GPOEO_STAT(i, t1_ - (t0));              \
+    t0 = t1_;                                              \
+  } while (0)
 #else
 #define GPOEO_STAT(i, v) ((void)0)
+#define GPOEO_TICK(i, t0) ((void)0)
 #endif
 constexpr int kWarps = kScoreThreads / 32;
 
@@ -369,7 +379,10 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 #define GPOEO_BUCKETS 32
 #endif
 #ifndef GPOEO_BUCKET_MINB
-#define GPOEO_BUCKET_MINB 16  // resident one-warp CTAs per SM the register budget targets
+#define GPOEO_BUCKET_MINB 14  // resident one-warp CTAs per SM the register budget targets (xl launch)
+#endif
+#ifndef GPOEO_BUCKET_MINB_MID
+#define GPOEO_BUCKET_MINB_MID 20  // the same for the mid launch (L <= kBucketSplitL, smaller regions)
 #endif
 constexpr int kBuckets = GPOEO_BUCKETS;
 constexpr int kBucketMaxL = 8192;
@@ -465,6 +478,9 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   constexpr int P = G * (G - 1) / 2;
   constexpr int KPL = kBuckets >= 32 ? kBuckets / 32 : 1;  // buckets per lane (lanes >= K idle if K < 32)
   // ---- range of W_i ----------------------------------------------------------------
+#ifdef GPOEO_STATS
+  long long tk = clock64();
+#endif
   float mnf = INFINITY, mxf = -INFINITY;
 #pragma unroll 4
   for (int s = lane; s < L; s += 32) {
@@ -483,20 +499,18 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // bucket of a value: any deterministic monotone map works (both sort loops use it)
   const float bscale = (float)kBuckets / (mxf - mnf);
   // ---- stable counting sort of sample indices by value bucket ------------------------
-  // Lane l owns the contiguous chunk [l*CH, (l+1)*CH): per-lane counts cnt[b][l], an
-  // exclusive scan in (bucket, lane) order, then each lane scatters its chunk in order. The
-  // result is sorted by (bucket, position): deterministic, no warp-synchronous multisplit.
+  // Lane l owns the samples s = l + 32 i (coalesced loads): per-lane counts cnt[b][l], an
+  // exclusive scan in (bucket, lane) order, then each lane scatters its samples in order.
+  // The result is sorted by (bucket, lane, i): deterministic, no warp-synchronous multisplit.
   auto bucket_of_v = [&](float v) -> int {
     const int b = (int)__fmul_rn(__fsub_rn(v, mnf), bscale);
     return b < 0 ? 0 : (b > kBuckets - 1 ? kBuckets - 1 : b);
   };
   auto bucket_of = [&](int s) -> int { return bucket_of_v(__ldg(A + s)); };
-  const int CH = (L + 31) >> 5;
-  const int c0 = lane * CH, c1 = (c0 + CH < L) ? c0 + CH : L;
 #pragma unroll
   for (int b = 0; b < kBuckets; ++b) bv.lcnt[b * 32 + lane] = 0;
 #pragma unroll 4
-  for (int s = c0; s < c1; ++s) {
+  for (int s = lane; s < L; s += 32) {
     const int b = bucket_of(s);
     bv.lcnt[b * 32 + lane] += 1;  // own column: no race
   }
@@ -539,13 +553,14 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     __syncwarp();
   }
 #pragma unroll 4
-  for (int s = c0; s < c1; ++s) {
+  for (int s = lane; s < L; s += 32) {
     const int b = bucket_of(s);
     const int slot = bv.lcnt[b * 32 + lane];
     bv.lcnt[b * 32 + lane] = (uint16_t)(slot + 1);
     bv.pos[slot] = (uint16_t)s;
   }
   __syncwarp();
+  GPOEO_TICK(8, tk);
   // ---- per-bucket range and shifted sums (one lane per bucket, slot order) ----------
 #pragma unroll 1
   for (int q = 0; q < KPL; ++q) {
@@ -574,6 +589,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     bv.blab[b] = 0xFE;
   }
   __syncwarp();
+  GPOEO_TICK(9, tk);
   // ---- CEM passes --------------------------------------------------------------------
   Cem<G> cem;
   cem.init(mn, R);
@@ -762,6 +778,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     mstep<G>(cem, v, L, 32, lane);
   }
   if (lane == 0) { GPOEO_STAT(0, 1); GPOEO_STAT(1, passes); }
+  GPOEO_TICK(10, tk);
   // ---- final groups on W_i and the same index sets on W_{i+1} (position order with
   // coalesced loads; the same loop for both windows, Z28). A sample's final label is its
   // bucket's state, or its own label when the bucket is mixed. -------------------------
@@ -793,6 +810,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     if (w[j] == 0.0) continue;
     num += w[j] * smape(w[G + j] / w[j] - mA, w[2 * G + j] / w[j] - mB);
   }
+  GPOEO_TICK(11, tk);
   return num / (double)L;
 }
 
@@ -951,8 +969,8 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
 
 // Bucket path (L >= kBucketMinL): kBucketWarps warps per CTA, one query per CTA at a
 // time, one pair per warp at a time (streaming path beyond bucket_lcap).
-template <int G>
-__global__ void __launch_bounds__(kBucketWarps * 32, GPOEO_BUCKET_MINB) score_bucket_kernel(ScoreArgs a) {
+template <int G, int MINB>
+__global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(ScoreArgs a) {
   __shared__ int64_t s_item;
   __shared__ double s_team[kBucketWarps];
   extern __shared__ __align__(16) uint8_t s_dyn[];  // kBucketWarps x BucketView regions
@@ -1013,6 +1031,18 @@ static int grid_of(K kern, int threads, size_t smem, int cap) {
   return g < cap ? g : cap;
 }
 
+template <int G, int MINB>
+static cudaError_t launch_bucket(ScoreArgs a, int lcap, cudaStream_t s) {
+  a.bucket_lcap = lcap;
+  const size_t smem = (size_t)kBucketWarps * bucket_region_bytes(lcap);
+  auto kern = score_bucket_kernel<G, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // label-scratch slots exist for kMaxScoreCtas * kWarps warps (gpoeo_api.cu layout)
+  kern<<<grid_of(kern, kBucketWarps * 32, smem, kMaxScoreCtas * kWarps / kBucketWarps), kBucketWarps * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int G>
 static cudaError_t launch_g(const ScoreArgs& base, const ItemList& list, int32_t min_L, int32_t max_L,
                             cudaStream_t s) {
@@ -1027,20 +1057,23 @@ static cudaError_t launch_g(const ScoreArgs& base, const ItemList& list, int32_t
     if (e != cudaSuccess) return e;
   }
   if (max_L >= kBucketMinL) {
+    // mid launch: kBucketMinL <= L <= kBucketSplitL from the back of `items`
     ScoreArgs a = base;
     a.count = list.n_big;
     a.cursor = list.cur_big;
     a.reverse = 1;
-    const int lcap = ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15;
-    a.bucket_lcap = lcap;
-    const size_t smem = (size_t)kBucketWarps * bucket_region_bytes(lcap);
-    auto kern = score_bucket_kernel<G>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int top = max_L < kBucketSplitL ? max_L : kBucketSplitL;
+    cudaError_t e = launch_bucket<G, GPOEO_BUCKET_MINB_MID>(a, (top + 15) & ~15, s);
     if (e != cudaSuccess) return e;
-    // label-scratch slots exist for kMaxScoreCtas * kWarps warps (gpoeo_api.cu layout)
-    score_bucket_kernel<G><<<grid_of(kern, kBucketWarps * 32, smem, kMaxScoreCtas * kWarps / kBucketWarps),
-                             kBucketWarps * 32, smem, s>>>(a);
-    e = cudaGetLastError();
+  }
+  if (max_L > kBucketSplitL) {
+    // xl launch: L > kBucketSplitL from `xl` (streaming path beyond kBucketMaxL)
+    ScoreArgs a = base;
+    a.items = list.xl;
+    a.count = list.n_xl;
+    a.cursor = list.cur_xl;
+    a.reverse = 0;
+    cudaError_t e = launch_bucket<G, GPOEO_BUCKET_MINB>(a, ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1075,9 +1108,9 @@ cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, do
 
 #ifdef GPOEO_STATS
 extern "C" __attribute__((visibility("default"))) int gpoeo_debug_stats(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, gpoeo::g_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return -5;
+  if (cudaMemcpyFromSymbol(out, gpoeo::g_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -5;
   if (reset) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(gpoeo::g_stats, z, sizeof(z));
   }
   return 0;

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--batch", type=int, default=2000)
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--first", type=int, default=0)
+    ap.add_argument("--maxit", type=int, default=32, help="CEM pass cap (timing experiments only)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -32,6 +33,7 @@ def main():
 
     spec = tg.CFG3.with_(batch=args.batch)
     p = g.params_for(spec)
+    p.gmm_max_iters = args.maxit
     x = torch.empty((args.batch, spec.n_features * spec.n_samples), dtype=torch.float32, device="cuda")
     tg.generate_device(spec, x, first=args.first, count=args.batch)
     ws = g.alloc_workspace(g.workspace_size(p, args.batch))
@@ -41,7 +43,7 @@ def main():
     out = {}
     for r in range(args.repeat):
         if stats_fn is not None:
-            buf = (ctypes.c_ulonglong * 8)()
+            buf = (ctypes.c_ulonglong * 16)()
             stats_fn(buf, 1)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         for e in evs:
@@ -51,14 +53,16 @@ def main():
         torch.cuda.synchronize()
         out["phase_ms"] = {n: evs[i].elapsed_time(evs[i + 1]) for i, n in enumerate(g.PHASES)}
         if stats_fn is not None:
-            buf = (ctypes.c_ulonglong * 8)()
+            buf = (ctypes.c_ulonglong * 16)()
             stats_fn(buf, 0)
             s = list(buf)
             out["stats"] = {"bucket_pairs": s[0], "bucket_passes_per_pair": s[1] / max(s[0], 1),
                             "swept_members_per_pass": s[2] / max(s[1], 1),
                             "straddle_members_per_pass": s[3] / max(s[1], 1),
                             "straddle_buckets_per_pass": s[4] / max(s[1], 1), "team_pairs": s[5],
-                            "team_passes_per_pair": s[6] / max(s[5], 1)}
+                            "team_passes_per_pair": s[6] / max(s[5], 1),
+                            "bucket_cycles_per_pair": {k: s[8 + i] / max(s[0], 1) for i, k in
+                                                       enumerate(["range_sort", "bucket_sums", "passes", "final"])}}
     out["counters"] = g.read_counters(ws, p, args.batch)
     # query mix from the per-trace detail (candidates + local ranges)
     _, det, _ = g.detect_periods(x, p, workspace=ws, detail=True)
