@@ -79,6 +79,18 @@ __device__ __forceinline__ double smape(double a, double b) {
   return den == 0.0 ? 0.0 : fabs(a - b) / den;
 }
 
+// 1/y to within ~1 ulp for finite normal y: MUFU reciprocal + two Newton steps (IEEE
+// division is a long software sequence; the scorer's divisions need no correct rounding:
+// the M-step and the root finder already differ from the oracle at rounding level, Z27).
+__device__ __forceinline__ double rcp_fast(double y) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  double e = fma(-y, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Team all-reduce of NV doubles (identical result in every lane of the team).
 // tau <= 32: xor butterfly. tau >= 64: warp butterfly, then per-warp sums through smem
 // (red[buf][warp][v]) added in warp order by lane v, then broadcast from lane v.
@@ -190,12 +202,12 @@ __device__ __forceinline__ void mstep(Cem<G>& cem, const double* v, int L, int t
       if (nj == 0.0) {
         c = -INFINITY;  // dead (stays dead)
       } else {
-        const double rn = 1.0 / nj;  // two divisions per component (not five)
+        const double rn = rcp_fast(nj);  // nj >= 1: two reciprocals per component, no division
         const double m = S * rn;
         const double dm = m - mu;
         double var = Q * rn - dm * dm;
         if (var < cem.floor_var) var = cem.floor_var;
-        h = 0.5 / var;
+        h = 0.5 * rcp_fast(var);  // var >= floor_var > 0
         const double p = nj * (1.0 / (double)L);
         mu = m;
         c = 0.5 * log(2.0 * p * p * h);  // ln pi - 1/2 ln var
@@ -463,9 +475,9 @@ __device__ __forceinline__ void score_crossings(double muj, double cj, double hj
   }
   const double sq = sqrt(D);
   const double q = -0.5 * (B + copysign(sq, B));
-  if (q != 0.0) {
-    r0 = m0 + q / A;
-    r1 = m0 + C / q;
+  if (q != 0.0) {  // |A| > 1e-13 scale here: both reciprocals are of normal numbers
+    r0 = m0 + q * rcp_fast(A);
+    r1 = m0 + C * rcp_fast(q);
   } else {
     r0 = m0 - B / (2.0 * A);
   }
@@ -652,6 +664,9 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;
+    int nc[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) nc[j] = 0;
     // classify this lane's buckets. A bucket with no envelope root within
     // [min - delta, max + delta] is whole: every member takes the label of the per-sample
     // rule at its minimum, statistics from the bucket sums. Its state records that label;
@@ -700,7 +715,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       for (int j = 0; j < G; ++j)
         if (lbl == j) {
           const double dc = c - cem.mu[j];
-          v[j] += n;
+          nc[j] += cnt;
           v[G + j] += n * c + a1;
           v[2 * G + j] += a2 + dc * (2.0 * a1 + n * dc);
         }
@@ -753,7 +768,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         const int lbl = cem.assign(y, it, e);
 #pragma unroll
         for (int j = 0; j < G; ++j)
-          if (lbl == j) { v[j] += 1.0; v[G + j] += y; v[2 * G + j] += e[j]; }
+          if (lbl == j) { nc[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
         const int st = bv.blab[b];  // previous state: uniform label, or mixed (per member)
         const int old = st < G ? st : (int)bv.lab[p];
         changed |= (int)(old != lbl);
@@ -771,10 +786,26 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         }
     }
     __syncwarp();
-    v[3 * G] = (double)changed;
     passes = it;
-    xor_sum_vec<NV>(v, 32);
-    if ((it > 1 && v[3 * G] == 0.0) || it == maxit) break;  // labels final
+    // warp sums: S_j, Q_j as doubles; the counts two per 32-bit word (n_j <= L < 2^16);
+    // "any label changed" as a vote
+    {
+      constexpr int NPK = (G + 1) / 2;
+      unsigned pk[NPK];
+#pragma unroll
+      for (int i = 0; i < NPK; ++i) pk[i] = (unsigned)nc[2 * i] | ((2 * i + 1 < G ? (unsigned)nc[2 * i + 1] : 0u) << 16);
+#pragma unroll 1
+      for (int off = 16; off; off >>= 1) {
+#pragma unroll
+        for (int i = 0; i < NPK; ++i) pk[i] += __shfl_xor_sync(FULL, pk[i], off);
+#pragma unroll
+        for (int i = G; i < 3 * G; ++i) v[i] += __shfl_xor_sync(FULL, v[i], off);
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) v[j] = (double)((pk[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+    }
+    const bool any_changed = __any_sync(FULL, changed);
+    if ((it > 1 && !any_changed) || it == maxit) break;  // labels final
     mstep<G>(cem, v, L, 32, lane);
   }
   if (lane == 0) { GPOEO_STAT(0, 1); GPOEO_STAT(1, passes); }
