@@ -243,12 +243,15 @@ def run_gpu(args) -> None:
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
 
     # dram traffic of the dominant kernel from the committed ncu --set full capture
-    traffic, traffic_note = None, None
+    # (profiles/ncu_traffic.json: DRAM bytes per trace from one `ncu --set full` capture, scaled to
+    # this batch; see profiles/README.md)
+    traffic, traffic_note, traffic_spec = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tj = json.load(f)
-        traffic = tj["dram_bytes_per_launch"]
+        traffic = tj["scorer_dram_bytes_per_trace"] * B
         traffic_note = tj.get("note")
+        traffic_spec = tj["spectral_only_dram_bytes_per_trace"] * B
     except Exception:
         pass
     # dominant kernel: the Alg. 2 scorer (two launches per step, candidate + local queries)
@@ -284,8 +287,36 @@ def run_gpu(args) -> None:
         "phase_ms": {n: float(v) for n, v in zip(g.PHASES, phase_ms)},
         "work_counters": counters,
         "clocks": clocks,
-        "gpu_launches": 8 * args.steps,  # composite, spectrum, 2x(team + bucket scorer), select, final
+        # fused spectrum (1), 2 x scorer (team, mid and xl bucketed: 3), select (1), final (1)
+        "gpu_launches": 9 * args.steps,
     }
+
+    # spectral-only detector (rows a1-a3 + arg-max, T_iter = 1/f_major) on
+    # the same resident traces: the HBM-bound path, 4*F*N bytes read per trace, 16 B written
+    if not args.no_spectral:
+        mws = g.alloc_workspace(g.major_workspace_size(p, B), dev)
+        mres = torch.empty(B * g.MAJOR_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        for _ in range(args.warmup):
+            g.detect_major_periods(x, p, workspace=mws, results=mres, stream=stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for _ in range(args.steps):
+            g.detect_major_periods(x, p, workspace=mws, results=mres, stream=stream)
+        m1.record(stream)
+        torch.cuda.synchronize()
+        mms = _max_over_ranks(m0.elapsed_time(m1), dev) / args.steps
+        mbytes = B * (4 * spec.n_features * spec.n_samples + g.MAJOR_DTYPE.itemsize)
+        mgbs = mbytes / (mms / 1e3) / 1e9
+        line["spectral_only"] = {
+            "metric": "traces/sec spectral-only period (T_iter = 1/f_major, P:291)", "value": world * B / (mms / 1e3),
+            "unit": "traces/s", "ms_per_step": mms, "kernel": "fused_spectrum_65536<3> (mode major), 1 launch/step",
+            "roofline": {"bound": "hbm", "achieved": mgbs, "peak": hbm_peak, "unit": "GB/s", "frac": mgbs / hbm_peak,
+                         "traffic": traffic_spec, "peak_kind": peak_kind,
+                         "bytes": f"{4 * spec.n_features * spec.n_samples + g.MAJOR_DTYPE.itemsize} B/trace"}}
+        del mws, mres
 
     # e2e: same metric through the public host entry point (pinned host buffers, H2D+D2H inside)
     del x
@@ -335,6 +366,7 @@ def main():
     ap.add_argument("--ref-traces", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-spectral", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
