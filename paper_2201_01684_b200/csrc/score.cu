@@ -398,7 +398,8 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 #endif
 constexpr int kBuckets = GPOEO_BUCKETS;
 constexpr int kBucketMaxL = 8192;
-constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order, no CTA barrier waits
+constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order (the range carry needs it)
+static_assert(kBucketWarps == 1, "pair_err_bucket's range carry assumes one warp walks a query's pairs in order");
 
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
   return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) + (size_t)kBuckets * 8 * 2 +
@@ -483,9 +484,11 @@ __device__ __forceinline__ void score_crossings(double muj, double cj, double hj
   }
 }
 
+// have_range: range = [min, max] of W_i, already seen by the previous pair's final pass; on
+// return range = [min, max] of W_{i+1} (this pair's final pass reads it), for the next pair.
 template <int G>
 __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int lane, BucketView bv, int maxit,
-                                  long long& passes_out) {
+                                  long long& passes_out, bool have_range, float2& range) {
   constexpr int NV = 3 * G + 1;
   constexpr int P = G * (G - 1) / 2;
   constexpr int KPL = kBuckets >= 32 ? kBuckets / 32 : 1;  // buckets per lane (lanes >= K idle if K < 32)
@@ -493,21 +496,42 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
 #ifdef GPOEO_STATS
   long long tk = clock64();
 #endif
-  float mnf = INFINITY, mxf = -INFINITY;
+  float mnf = range.x, mxf = range.y;
+  if (!have_range) {
+    mnf = INFINITY;
+    mxf = -INFINITY;
 #pragma unroll 4
-  for (int s = lane; s < L; s += 32) {
-    const float v = __ldg(A + s);
-    mnf = fminf(mnf, v);
-    mxf = fmaxf(mxf, v);
-  }
+    for (int s = lane; s < L; s += 32) {
+      const float v = __ldg(A + s);
+      mnf = fminf(mnf, v);
+      mxf = fmaxf(mxf, v);
+    }
 #pragma unroll 1
-  for (int off = 16; off; off >>= 1) {
-    mnf = fminf(mnf, __shfl_xor_sync(FULL, mnf, off));
-    mxf = fmaxf(mxf, __shfl_xor_sync(FULL, mxf, off));
+    for (int off = 16; off; off >>= 1) {
+      mnf = fminf(mnf, __shfl_xor_sync(FULL, mnf, off));
+      mxf = fmaxf(mxf, __shfl_xor_sync(FULL, mxf, off));
+    }
   }
   const double mn = (double)mnf, mx = (double)mxf;  // exact
   const double R = mx - mn;
-  if (!(R > 0.0) || G == 1) return 0.0;
+  if (!(R > 0.0) || G == 1) {
+    // constant window (Z13: e_i = 0); the next pair still needs the range of W_{i+1}
+    const float* B = A + L;
+    float nmn = INFINITY, nmx = -INFINITY;
+#pragma unroll 4
+    for (int p = lane; p < L; p += 32) {
+      const float v = __ldg(B + p);
+      nmn = fminf(nmn, v);
+      nmx = fmaxf(nmx, v);
+    }
+#pragma unroll 1
+    for (int off = 16; off; off >>= 1) {
+      nmn = fminf(nmn, __shfl_xor_sync(FULL, nmn, off));
+      nmx = fmaxf(nmx, __shfl_xor_sync(FULL, nmx, off));
+    }
+    range = make_float2(nmn, nmx);
+    return 0.0;
+  }
   // bucket of a value: any deterministic monotone map works (both sort loops use it)
   const float bscale = (float)kBuckets / (mxf - mnf);
   // ---- stable counting sort of sample indices by value bucket ------------------------
@@ -818,10 +842,13 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   for (int i = 0; i < NV; ++i) w[i] = 0.0;
   double TA = 0.0;
   const float* B = A + L;
+  float nmn = INFINITY, nmx = -INFINITY;  // range of W_{i+1}, handed to the next pair
 #pragma unroll 4
   for (int p = lane; p < L; p += 32) {
-    const float fa = __ldg(A + p);
-    const double ya = (double)fa, yb = (double)__ldg(B + p);
+    const float fa = __ldg(A + p), fb = __ldg(B + p);
+    const double ya = (double)fa, yb = (double)fb;
+    nmn = fminf(nmn, fb);
+    nmx = fmaxf(nmx, fb);
     TA += ya;
     w[3 * G] += yb;
     int l = bv.blab[bucket_of_v(fa)];
@@ -832,7 +859,12 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   }
   xor_sum_vec<NV>(w, 32);
 #pragma unroll 1
-  for (int off = 16; off; off >>= 1) TA += __shfl_xor_sync(FULL, TA, off);
+  for (int off = 16; off; off >>= 1) {
+    TA += __shfl_xor_sync(FULL, TA, off);
+    nmn = fminf(nmn, __shfl_xor_sync(FULL, nmn, off));
+    nmx = fmaxf(nmx, __shfl_xor_sync(FULL, nmx, off));
+  }
+  range = make_float2(nmn, nmx);
   if (lane == 0) passes_out += (long long)(passes + 1) * L;
   const double mA = TA / (double)L, mB = w[3 * G] / (double)L;
   double num = 0.0;
@@ -1022,8 +1054,10 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
     double acc = 0.0;
     if (L <= a.bucket_lcap) {
       BucketView bv = BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap), a.bucket_lcap);
+      float2 range = make_float2(0.f, 0.f);
       for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
-        acc += pair_err_bucket<G>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes);
+        // kBucketWarps == 1: pairs in order, so the previous final pass saw this W_i
+        acc += pair_err_bucket<G>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes, pidx != warp, range);
         __syncwarp();
       }
     } else {
