@@ -79,6 +79,14 @@ class OrMajor(ctypes.Structure):
                 ("d_major", ctypes.c_double), ("d_peak", ctypes.c_double)]
 
 
+class OrRolling(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("t_init", ctypes.c_int32), ("t_iter", ctypes.c_int32),
+                ("n_sub", ctypes.c_int32), ("early", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("err_init", ctypes.c_double), ("err_iter", ctypes.c_double), ("diff", ctypes.c_double),
+                ("smpdur_next", ctypes.c_double), ("sub_start", ctypes.c_int32 * 64),
+                ("sub_period", ctypes.c_int32 * 64), ("sub_err", ctypes.c_double * 64)]
+
+
 def build() -> str:
     """Compile the oracle (gcc, fp64, no FMA contraction). Building the checker is not using it."""
     if not (os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC)):
@@ -118,6 +126,10 @@ def _L():
         lib.oracle_major.argtypes = [P, ctypes.POINTER(OrParams), P, ctypes.POINTER(OrMajor)]
         lib.oracle_major.restype = ctypes.c_int
         assert lib.oracle_sizeof_major() == ctypes.sizeof(OrMajor)
+        lib.oracle_rolling.argtypes = [P, ctypes.POINTER(OrParams), P, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, ctypes.POINTER(OrRolling)]
+        lib.oracle_rolling.restype = ctypes.c_int
+        assert lib.oracle_sizeof_rolling() == ctypes.sizeof(OrRolling)
         assert lib.oracle_sizeof_params() == ctypes.sizeof(OrParams)
         assert lib.oracle_sizeof_result() == ctypes.sizeof(OrResult)
         _lib = lib
@@ -334,3 +346,32 @@ def major_batch(X: np.ndarray, params: Params, threads: int | None = None) -> li
     threads = threads or os.cpu_count() or 1
     with ThreadPoolExecutor(max_workers=threads) as ex:
         return list(ex.map(lambda b: major(X[b], params), range(X.shape[0])))
+
+
+@dataclass
+class Rolling:
+    """R1: Alg. 3 on one recorded trace (reading R5). Periods in samples."""
+    status: int
+    t_init: int
+    t_iter: int
+    early: bool
+    diff: float
+    smpdur_next: float
+    sub_start: list
+    sub_period: list
+    sub_err: list
+
+
+def rolling(x: np.ndarray, params: Params, c_measure: float = 2.0, step: float = 0.5, c_eval: float = 6.5,
+            diff_threshold: float = 0.05) -> Rolling:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    p = params.c()
+    r = OrRolling()
+    w = None if params.weights is None else np.asarray(params.weights, np.float32).astype(np.float64)
+    if _L().oracle_rolling(_ptr(x), ctypes.byref(p), None if w is None else _ptr(w), c_measure, step, c_eval,
+                           diff_threshold, ctypes.byref(r)) != 0:
+        raise ValueError("oracle_rolling: invalid parameters")
+    n = r.n_sub
+    return Rolling(status=r.status, t_init=r.t_init, t_iter=r.t_iter, early=bool(r.early), diff=r.diff,
+                   smpdur_next=r.smpdur_next, sub_start=list(r.sub_start[:n]), sub_period=list(r.sub_period[:n]),
+                   sub_err=list(r.sub_err[:n]))

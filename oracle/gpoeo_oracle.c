@@ -26,6 +26,7 @@
  *   O8 margins (Z27) and work counters
  *   O9 exhaustive search (tests only)
  *   S1 spectral-only detector (T_iter = 1/f_major)
+ *   R1 Alg. 3 rolling detector on a recorded trace
  *
  * Pins (tests/test_oracle_*.py): O1 closed-form z-scores; O2 numpy.fft.rfft,
  * Parseval, pure tones, impulse; O3 hand spectra and scipy find_peaks;
@@ -599,6 +600,116 @@ done:
   return 0;
 }
 int oracle_sizeof_major(void) { return (int)sizeof(or_major); }
+
+/* ------------------------------------------------------------------------ */
+/* R1. Alg. 3, the online robust period detection framework
+ * (P:383-429), on one recorded trace. Reading R5:
+ *  - Smp is the composite feature sequence: y = O1(x) once over the trace; a
+ *    SubSmp = {s_istart .. s_N} is a suffix of y, and "Algorithm1(SubSmp)" is Alg. 1 on it
+ *    as a one-channel sequence of its own length N_j (its z-score is an affine map of the
+ *    suffix: Z1), with L_max clipped to floor(N_j/2) (Z21);
+ *  - times in samples (T_s scales out, Z25): SmpDur = N - 1, T_init = L_init;
+ *    t_start = max(0, SmpDur - (2 + c_eval step) T_init), advanced by step T_init while
+ *    (SmpDur - t_start)/T_init >= c_measure; istart = 1 + floor(t_start) (1-based);
+ *  - lines 3-6 end the call (the "return" the text describes; Z24);
+ *  - only suffixes whose Alg. 1 finds a period enter T and Err; T_iter = T_k of the
+ *    smallest err (ties: smaller T, Z17); Diff = |max T - min T| / mean T;
+ *    Diff < Diff_threshold -> SmpDur_next = -1, else ceil(SmpDur/max T) max T - SmpDur;
+ *    no suffix with a period -> T_iter = T_init, SmpDur_next = c_measure T_init (keep sampling);
+ *  - c_measure = 2, step = 0.5, c_eval = 6.5; Diff_threshold = 0.05 (the paper
+ *    gives no value).
+ * Status: Alg. 1's status on the whole trace (no rolling when it is not OK). */
+#define OR_ROLL_MAX 64
+typedef struct {
+  int32_t status;
+  int32_t t_init;           /* L_init of Alg. 1 on the whole trace                       */
+  int32_t t_iter;           /* T_iter (samples)                                          */
+  int32_t n_sub;            /* suffixes evaluated                                        */
+  int32_t early;            /* 1: lines 3-6 ended the call                               */
+  int32_t pad;
+  double err_init;
+  double err_iter;
+  double diff;
+  double smpdur_next;       /* samples; -1 = stop sampling                               */
+  int32_t sub_start[OR_ROLL_MAX]; /* 0-based start of each suffix                       */
+  int32_t sub_period[OR_ROLL_MAX];/* T_j (-1 if Alg. 1 found none)                       */
+  double sub_err[OR_ROLL_MAX];
+} or_rolling;
+
+int oracle_rolling(const float* x, const or_params* p, const double* weights, double c_measure, double step,
+                   double c_eval, double diff_threshold, or_rolling* out) {
+  memset(out, 0, sizeof(*out));
+  const int32_t N = p->n_samples;
+  or_result r;
+  if (oracle_detect(x, p, weights, &r, NULL) != 0) return -1;
+  out->status = r.status;
+  out->t_init = r.period;
+  out->err_init = r.error;
+  out->t_iter = -1;
+  out->smpdur_next = -1.0;
+  if (r.status != OR_TRACE_OK) return 0;
+  const double L0 = (double)r.period;
+  const double smpdur = (double)(N - 1);
+  if (smpdur < c_measure * L0) {
+    out->early = 1;
+    out->t_iter = r.period;
+    out->err_iter = r.error;
+    out->smpdur_next = c_measure * L0 - smpdur;
+    return 0;
+  }
+  float* y = (float*)malloc(sizeof(float) * N);
+  oracle_composite(x, N, p->n_features, weights, y, NULL, NULL);
+  double t_start = smpdur - (2.0 + c_eval * step) * L0;
+  if (t_start < 0.0) t_start = 0.0;
+  int n = 0;
+  while ((smpdur - t_start) / L0 >= c_measure && n < OR_ROLL_MAX) {
+    const int32_t s0 = (int32_t)floor(t_start); /* istart - 1 */
+    const int32_t Nj = N - s0;
+    or_params q = *p;
+    q.n_samples = Nj;
+    q.n_features = 1;
+    if (q.max_period > Nj / 2) q.max_period = Nj / 2;
+    or_result rj;
+    out->sub_start[n] = s0;
+    out->sub_period[n] = -1;
+    out->sub_err[n] = 0.0;
+    if (q.min_period <= q.max_period && oracle_detect(y + s0, &q, NULL, &rj, NULL) == 0 && rj.status == OR_TRACE_OK) {
+      out->sub_period[n] = rj.period;
+      out->sub_err[n] = rj.error;
+    }
+    ++n;
+    t_start += step * L0;
+  }
+  out->n_sub = n;
+  int k = -1;
+  double tmin = 0.0, tmax = 0.0, tsum = 0.0;
+  int cnt = 0;
+  for (int j = 0; j < n; ++j) {
+    if (out->sub_period[j] < 0) continue;
+    const double T = (double)out->sub_period[j];
+    if (k < 0 || out->sub_err[j] < out->sub_err[k] ||
+        (out->sub_err[j] == out->sub_err[k] && out->sub_period[j] < out->sub_period[k]))
+      k = j;
+    if (cnt == 0 || T < tmin) tmin = T;
+    if (cnt == 0 || T > tmax) tmax = T;
+    tsum += T;
+    ++cnt;
+  }
+  if (k < 0) {
+    out->t_iter = r.period;
+    out->err_iter = r.error;
+    out->diff = INFINITY;
+    out->smpdur_next = c_measure * L0;
+  } else {
+    out->t_iter = out->sub_period[k];
+    out->err_iter = out->sub_err[k];
+    out->diff = fabs((tmax - tmin) / (tsum / cnt));
+    out->smpdur_next = out->diff < diff_threshold ? -1.0 : ceil(smpdur / tmax) * tmax - smpdur;
+  }
+  free(y);
+  return 0;
+}
+int oracle_sizeof_rolling(void) { return (int)sizeof(or_rolling); }
 
 /* O9 (tests only): Err(L) for every L in [L_min, L_max] of an already-formed
  * signal y; returns the global argmin (Err, L). */

@@ -33,7 +33,7 @@
 namespace gpoeo {
 
 #ifndef GPOEO_SCORE_MINB
-#define GPOEO_SCORE_MINB 2  // resident CTAs per SM the register budget is sized for
+#define GPOEO_SCORE_MINB 3  // resident CTAs per SM the register budget is sized for (80 regs; 3 beats 2)
 #endif
 
 constexpr unsigned FULL = 0xffffffffu;
