@@ -167,6 +167,22 @@ def test_similarity_groups_and_caps(G, maxit):
         assert (got == 0).all()
 
 
+def test_similarity_long_windows_all_paths():
+    # every scorer path on one signal: team (L < 513), mid bucketed (<= 2048), xl bucketed
+    # (<= 8192) and the streaming warp path (L > 8192, labels in global scratch)
+    x = tg.generate_host(tg.CFG2.with_(n_samples=32768, period_lo=3000.0, period_hi=9000.0), 0, 2)
+    ys = np.stack([O.composite(x[b])[0] for b in range(2)])
+    Ls = [100, 1200, 3000, 8192, 8193, 10000, 16384]
+    ti = np.repeat(np.arange(2), len(Ls)).astype(np.int32)
+    pe = np.tile(np.array(Ls, np.int32), 2)
+    got = g.similarity_error(torch.from_numpy(ys).cuda(), ti, pe).cpu().numpy()
+    for q in range(len(ti)):
+        ref, margin = O.similarity_error(ys[ti[q]], int(pe[q]), with_margin=True)
+        if margin < 1e-10:
+            continue
+        assert abs(got[q] - ref) <= 1e-4 * max(ref, 1e-6), (ti[q], pe[q], got[q], ref)
+
+
 def test_similarity_exact_zero_on_periodic():
     rng = np.random.default_rng(5)
     rows, Ls = [], []
