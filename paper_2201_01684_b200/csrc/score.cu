@@ -26,7 +26,6 @@
 //  * L > 16*256: a warp owns the pair and streams samples from L1/L2 every pass (labels in
 //    shared memory or global scratch).
 //  * Err(L) is the sum of per-team partial sums in team order: deterministic.
-#include <stdlib.h>
 
 #include "gpoeo_internal.cuh"
 
