@@ -396,6 +396,8 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 #define GPOEO_BUCKET_MINB_MID 20  // the same for the mid launch (L <= kBucketSplitL, smaller regions)
 #endif
 constexpr int kBuckets = GPOEO_BUCKETS;
+static_assert((kBuckets <= 32 || kBuckets % 32 == 0) && kBuckets <= 255,
+              "a lane owns kBuckets/32 whole buckets; the flag word keeps the bucket in 8 bits");
 constexpr int kBucketMaxL = 8192;
 constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order (the range carry needs it)
 static_assert(kBucketWarps == 1, "pair_err_bucket's range carry assumes one warp walks a query's pairs in order");
