@@ -571,21 +571,9 @@ __device__ __forceinline__ void pass(float2* buf, const float2* tw, int Ns) {
   __syncthreads();
 }
 
-__device__ __forceinline__ double block_sum512(double v, double* red) {
-  for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < kT / 32; ++i) s += red[i];
-  return s;
-}
-
 struct FusedShared {
   PeakShared ps;
-  double red[kT / 32];
+  double red[kT / 32 * 2 * GPOEO_MAX_FEATURES];
   double stat[2][GPOEO_MAX_FEATURES][2];  // [rank][channel][sum, shifted sum of squares]
   float pm[2];                            // per-rank in-band peak maximum
   int32_t pk[2];                          // per-rank bin of that maximum (major mode)
@@ -660,6 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
   for (int64_t t = cid; t < p.batch; t += nclusters) {
     const float* xt = x + t * p.stride;
     // ---- A: stats over my quarter blocks {q, 2 + q} -----------------------------------
+    double sv[2 * F];  // [sum, shifted sum of squares] per channel
 #pragma unroll
     for (int c = 0; c < F; ++c) {
       const float* xc = xt + (int64_t)c * kN;
@@ -681,13 +670,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
         const double d0 = v0 - x0, d1 = v1 - x0, d2 = v2 - x0, d3 = v3 - x0;
         qq = __fma_rn(d0, d0, qq); qq = __fma_rn(d1, d1, qq); qq = __fma_rn(d2, d2, qq); qq = __fma_rn(d3, d3, qq);
       }
-      s = block_sum512(s, fs.red);
-      qq = block_sum512(qq, fs.red);
-      if (threadIdx.x == 0) {
-        fs.stat[q][c][0] = s;
-        fs.stat[q][c][1] = qq;
-        pfs->stat[q][c][0] = s;
-        pfs->stat[q][c][1] = qq;
+      sv[2 * c] = s;
+      sv[2 * c + 1] = qq;
+    }
+    // one block reduction for every channel: warp butterflies, then warps in index order
+    {
+#pragma unroll
+      for (int off = 16; off; off >>= 1)
+#pragma unroll
+        for (int i = 0; i < 2 * F; ++i) sv[i] += __shfl_xor_sync(0xffffffffu, sv[i], off);
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < 2 * F; ++i) fs.red[warp * 2 * GPOEO_MAX_FEATURES + i] = sv[i];
+      __syncthreads();
+      if (threadIdx.x < 2 * F) {
+        double a = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < kT / 32; ++w2) a += fs.red[w2 * 2 * GPOEO_MAX_FEATURES + threadIdx.x];
+        const int c = threadIdx.x >> 1, k = threadIdx.x & 1;
+        fs.stat[q][c][k] = a;
+        pfs->stat[q][c][k] = a;
       }
     }
     cluster.sync();
