@@ -341,10 +341,23 @@ def run_gpu(args) -> None:
         for _ in range(args.e2e_steps):
             g.detect_periods_host(xh, p, chunk=args.chunk, workspace=hws, out=out)
         te = _max_over_ranks(time.perf_counter() - t0, dev)
+        # the bound of this leg: a plain pinned H2D copy of one chunk (CUDA events)
+        dchunk = torch.empty((min(args.chunk, Be), xh.shape[1]), dtype=torch.float32, device=dev)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dchunk.copy_(xh[:dchunk.shape[0]], non_blocking=True)
+        c0.record()
+        for _ in range(3):
+            dchunk.copy_(xh[:dchunk.shape[0]], non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        h2d_gbs = 3 * dchunk.numel() * 4 / (c0.elapsed_time(c1) / 1e3) / 1e9
+        del dchunk
+        tbytes = spec.n_features * spec.n_samples * 4
         line["e2e"] = {"value": world * Be * args.e2e_steps / te, "unit": "traces/s",
-                       "h2d_bytes_per_step": Be * spec.n_features * spec.n_samples * 4,
+                       "h2d_bytes_per_step": Be * tbytes,
                        "d2h_bytes_per_step": Be * g.RESULT_DTYPE.itemsize,
                        "batch_per_gpu": Be, "chunk": args.chunk, "steps": args.e2e_steps,
+                       "h2d_copy_GBps": h2d_gbs, "h2d_bound_traces_per_s": world * h2d_gbs * 1e9 / tbytes,
                        "api": "gpoeo_detect_periods_host (pinned host traces, results to host, wall clock incl. sync)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(spec, args.cpu_traces, os.cpu_count() or 1)
@@ -361,7 +374,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-batch", type=int, default=16384)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--chunk", type=int, default=4096)
+    ap.add_argument("--chunk", type=int, default=2048)
     ap.add_argument("--cpu-traces", type=int, default=48)
     ap.add_argument("--ref-traces", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")

@@ -139,8 +139,10 @@ int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_p
  *  host_traces  HOST [batch][trace_stride] fp32 (pinned memory gives async overlap);
  *  host_results HOST [batch] gpoeo_result.
  * Streams chunks of `chunk` traces through the workspace (size it with
- * gpoeo_workspace_size_host), overlapping H2D copies with compute on an internal copy
- * stream, and SYNCHRONISES `stream` before returning (results are on the host). */
+ * gpoeo_workspace_size_host: three chunk buffers in flight), overlapping H2D copies with
+ * compute on an internal copy stream and two compute streams; result copies are issued three
+ * chunks late so a pageable host_results never stalls the pipeline. SYNCHRONISES `stream`
+ * before returning (results are on the host). */
 size_t gpoeo_workspace_size_host(const gpoeo_params* p, int64_t chunk);
 int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpoeo_params* p,
                               gpoeo_result* host_results, int64_t chunk, void* workspace, size_t workspace_bytes,

@@ -266,13 +266,19 @@ int gpoeo_detect_periods(const float* traces, int64_t batch, const gpoeo_params*
   return gpoeo_detect_periods_ex(traces, batch, p, results, nullptr, workspace, workspace_bytes, stream);
 }
 
+// gpoeo_detect_periods_host: chunk buffers (traces, results, workspace) in flight. Three, so
+// the copy of chunk c + 3 can start as soon as chunk c is done while chunks c + 1 and c + 2
+// compute (with two, both compute streams tended to finish together and the next copy then
+// left the GPU idle).
+constexpr int kHostBuffers = 3;
+
 size_t gpoeo_workspace_size_host(const gpoeo_params* p, int64_t chunk) {
   if (validate(p) != GPOEO_OK || chunk < 1) return 0;
   const Plan pl = make_plan(p, chunk);
   const size_t inner = layout(pl).total;
   const size_t tr = align_up(sizeof(float) * (size_t)p->trace_stride * (size_t)chunk);
   const size_t rs = align_up(sizeof(gpoeo_result) * (size_t)chunk);
-  return 2 * tr + 2 * rs + 2 * inner;
+  return kHostBuffers * (tr + rs + inner);
 }
 
 int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpoeo_params* p,
@@ -292,21 +298,25 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
   const size_t tr = align_up(sizeof(float) * (size_t)p->trace_stride * (size_t)chunk);
   const size_t rs = align_up(sizeof(gpoeo_result) * (size_t)chunk);
   char* base = static_cast<char*>(workspace);
-  float* dtr[2] = {reinterpret_cast<float*>(base), reinterpret_cast<float*>(base + tr)};
-  gpoeo_result* dres[2] = {reinterpret_cast<gpoeo_result*>(base + 2 * tr),
-                           reinterpret_cast<gpoeo_result*>(base + 2 * tr + rs)};
-  void* dws[2] = {base + 2 * tr + 2 * rs, base + 2 * tr + 2 * rs + inner};
+  float* dtr[kHostBuffers];
+  gpoeo_result* dres[kHostBuffers];
+  void* dws[kHostBuffers];
+  for (int i = 0; i < kHostBuffers; ++i) {
+    dtr[i] = reinterpret_cast<float*>(base + (size_t)i * tr);
+    dres[i] = reinterpret_cast<gpoeo_result*>(base + (size_t)kHostBuffers * tr + (size_t)i * rs);
+    dws[i] = base + (size_t)kHostBuffers * (tr + rs) + (size_t)i * inner;
+  }
   // one copy stream + two compute streams (the caller's and an internal one): chunk c uses
-  // buffer / workspace / stream c & 1, so copies overlap compute and the two chunks in flight
-  // fill each other's phase tails
+  // buffer c % 3 and compute stream c & 1, so copies overlap compute and the two chunks in
+  // flight fill each other's phase tails
   cudaStream_t cs, s2;
-  cudaEvent_t copied[2], done[2], start, fin;
+  cudaEvent_t copied[kHostBuffers], done[kHostBuffers], start, fin;
   if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return GPOEO_ERR_CUDA;
   if (cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
     cudaStreamDestroy(cs);
     return GPOEO_ERR_CUDA;
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kHostBuffers; ++i) {
     cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
   }
@@ -319,30 +329,43 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
   cudaStreamWaitEvent(cs, start, 0);
   cudaStreamWaitEvent(s2, start, 0);
   const int64_t nchunks = (batch + chunk - 1) / chunk;
-  for (int64_t c = 0; c < nchunks && rc == GPOEO_OK; ++c) {
-    const int b = (int)(c & 1);
+  // results of chunk c leave through the copy stream when buffer c % 3 is reused (or at the
+  // end): a D2H copy into pageable host memory blocks the host until it completes, so it is
+  // issued three chunks late, while the two chunks after it keep the GPU busy
+  auto drain = [&](int64_t c) -> int {
+    const int b = (int)(c % kHostBuffers);
     const int64_t first = c * chunk;
     const int64_t n = batch - first < chunk ? batch - first : chunk;
-    if (c >= 2) cudaStreamWaitEvent(cs, done[b], 0);  // buffer b free again
-    if (cudaMemcpyAsync(dtr[b], host_traces + first * p->trace_stride, sizeof(float) * (size_t)p->trace_stride * n,
+    if (cudaStreamWaitEvent(cs, done[b], 0) != cudaSuccess) return GPOEO_ERR_CUDA;
+    if (cudaMemcpyAsync(host_results + first, dres[b], sizeof(gpoeo_result) * n, cudaMemcpyDeviceToHost, cs) !=
+        cudaSuccess)
+      return GPOEO_ERR_CUDA;
+    return GPOEO_OK;
+  };
+  for (int64_t c = 0; c < nchunks && rc == GPOEO_OK; ++c) {
+    const int b = (int)(c % kHostBuffers);
+    cudaStream_t cstr = cst[c & 1];
+    const int64_t first = c * chunk;
+    const int64_t n = batch - first < chunk ? batch - first : chunk;
+    if (c >= kHostBuffers) rc = drain(c - kHostBuffers);  // buffer b free again once drained
+    if (rc == GPOEO_OK &&
+        cudaMemcpyAsync(dtr[b], host_traces + first * p->trace_stride, sizeof(float) * (size_t)p->trace_stride * n,
                         cudaMemcpyHostToDevice, cs) != cudaSuccess)
       rc = GPOEO_ERR_CUDA;
     cudaEventRecord(copied[b], cs);
-    cudaStreamWaitEvent(cst[b], copied[b], 0);
+    cudaStreamWaitEvent(cstr, copied[b], 0);
     const Plan pl = make_plan(p, n);
     const Layout L = layout(pl);
-    if (rc == GPOEO_OK) rc = run_detect(dtr[b], pl, L, dws[b], dres[b], nullptr, cst[b]);
-    if (rc == GPOEO_OK &&
-        cudaMemcpyAsync(host_results + first, dres[b], sizeof(gpoeo_result) * n, cudaMemcpyDeviceToHost, cst[b]) !=
-            cudaSuccess)
-      rc = GPOEO_ERR_CUDA;
-    cudaEventRecord(done[b], cst[b]);
+    if (rc == GPOEO_OK) rc = run_detect(dtr[b], pl, L, dws[b], dres[b], nullptr, cstr);
+    cudaEventRecord(done[b], cstr);
   }
-  cudaEventRecord(fin, s2);
+  for (int64_t c = nchunks > kHostBuffers ? nchunks - kHostBuffers : 0; c < nchunks && rc == GPOEO_OK; ++c)
+    rc = drain(c);
+  cudaEventRecord(fin, cs);  // every result copy, hence every chunk, is done
   cudaStreamWaitEvent(s, fin, 0);
   if (cudaStreamSynchronize(s) != cudaSuccess) rc = GPOEO_ERR_CUDA;
   cudaStreamSynchronize(cs);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kHostBuffers; ++i) {
     cudaEventDestroy(copied[i]);
     cudaEventDestroy(done[i]);
   }
