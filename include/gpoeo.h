@@ -45,7 +45,9 @@ extern "C" {
 typedef enum {
   GPOEO_OK = 0,
   GPOEO_ERR_INVALID_ARGUMENT = -1, /* a parameter is out of range or a pointer is NULL   */
-  GPOEO_ERR_UNSUPPORTED = -2,      /* N not a power of two in [2^3, 2^18]                */
+  GPOEO_ERR_UNSUPPORTED = -2,      /* N outside [2^3, 2^18]; or N not a power of two with a
+                                      band of more than ~50K bins (the band-limited DFT keeps
+                                      it in shared memory)                                  */
   GPOEO_ERR_WORKSPACE = -3,        /* workspace NULL or smaller than gpoeo_workspace_size */
   GPOEO_ERR_MISALIGNED = -4,       /* traces/workspace not 16-B aligned, stride % 4 != 0  */
   GPOEO_ERR_CUDA = -5              /* no device / launch failure                          */
@@ -60,7 +62,10 @@ typedef enum {
 
 /* Parameters of Alg. 1/2 for one call (every trace of the batch shares them). */
 typedef struct {
-  int32_t n_samples;      /* N, samples per trace: power of two, 2^3..2^18                  */
+  int32_t n_samples;      /* N, samples per trace, 2^3..2^18. Powers of two take the FFT path
+                             (Stockham, cluster FFT for N >= 2^16, one fused kernel at 2^16);
+                             other N the band-limited DFT (the definition at the bins the peak
+                             rule reads, O(N x bins): moderate N)                           */
   int32_t n_features;     /* F, feature channels per trace (power, SM util, mem util: P:459),
                              1..8                                                            */
   int64_t trace_stride;   /* floats between consecutive traces, >= F*N, multiple of 4       */

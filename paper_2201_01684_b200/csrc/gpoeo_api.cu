@@ -36,10 +36,12 @@ void local_range(int64_t N, int64_t kb, int64_t Lmin, int64_t Lmax, int64_t* lo,
   *hi = h;
 }
 
+Plan make_plan(const gpoeo_params* p, int64_t batch);
+constexpr size_t kBandSmemMax = 200 * 1024;  // dynamic shared memory the band kernel may use
+
 int validate(const gpoeo_params* p) {
   if (!p) return GPOEO_ERR_INVALID_ARGUMENT;
-  if (!is_pow2(p->n_samples) || p->n_samples < (1 << GPOEO_MIN_LOG2N) || p->n_samples > (1 << GPOEO_MAX_LOG2N))
-    return GPOEO_ERR_UNSUPPORTED;
+  if (p->n_samples < (1 << GPOEO_MIN_LOG2N) || p->n_samples > (1 << GPOEO_MAX_LOG2N)) return GPOEO_ERR_UNSUPPORTED;
   if (p->n_features < 1 || p->n_features > GPOEO_MAX_FEATURES) return GPOEO_ERR_INVALID_ARGUMENT;
   if (p->trace_stride < (int64_t)p->n_features * p->n_samples) return GPOEO_ERR_INVALID_ARGUMENT;
   if (p->trace_stride % 4 != 0) return GPOEO_ERR_MISALIGNED;
@@ -50,6 +52,8 @@ int validate(const gpoeo_params* p) {
   if (p->max_candidates < 1 || p->max_candidates > GPOEO_MAX_CANDIDATES) return GPOEO_ERR_INVALID_ARGUMENT;
   if (p->num_groups < 1 || p->num_groups > GPOEO_MAX_GROUPS) return GPOEO_ERR_INVALID_ARGUMENT;
   if (p->gmm_max_iters < 1 || p->gmm_max_iters > 1000000) return GPOEO_ERR_INVALID_ARGUMENT;
+  // N not a power of two: the band-limited DFT holds the band in shared memory
+  if (!is_pow2(p->n_samples) && band_smem_bytes(make_plan(p, 0), false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
   return GPOEO_OK;
 }
 
@@ -58,7 +62,7 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
   memset(&pl, 0, sizeof(pl));
   pl.N = p->n_samples;
   pl.F = p->n_features;
-  pl.log2N = ilog2(pl.N);
+  pl.log2N = is_pow2(pl.N) ? ilog2(pl.N) : -1;  // -1: the band-limited DFT path (spectrum.cu)
   pl.n = pl.N / 2;
   pl.C = pl.n > 16384 ? pl.n / 16384 : 1;
   pl.n2 = pl.n / pl.C;
@@ -185,7 +189,8 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   CK(mark(1));
   if (pl.batch > 0) {
     if (fused) CK(launch_spectral_fused(pl, traces, w, w.y, nullptr, kPeaksCandidates, s));
-    else CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
+    else if (is_pow2(pl.N)) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
+    else CK(launch_spectrum_band(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
   }
   CK(mark(2));
   if (pl.batch > 0)
@@ -388,6 +393,7 @@ int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params*
   if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace) || (signal && !aligned16(signal)))
     return GPOEO_ERR_MISALIGNED;
   if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  if (!is_pow2(pl.N) && spectra && band_smem_bytes(pl, true) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Work w = carve(pl, L, workspace);
   if (batch == 0) return GPOEO_OK;
@@ -397,7 +403,10 @@ int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params*
     return GPOEO_OK;
   }
   CK(launch_composite(traces, pl, y, w.status, s));
-  if (spectra) CK(launch_spectrum(pl, y, w.status, w, spectra, kPeaksNone, s));
+  if (spectra) {
+    if (is_pow2(pl.N)) CK(launch_spectrum(pl, y, w.status, w, spectra, kPeaksNone, s));
+    else CK(launch_spectrum_band(pl, y, w.status, w, spectra, kPeaksNone, s));
+  }
   return GPOEO_OK;
 }
 
@@ -433,7 +442,8 @@ int gpoeo_detect_major_periods(const float* traces, int64_t batch, const gpoeo_p
   w.y = reinterpret_cast<float*>(b);
   w.status = reinterpret_cast<int32_t*>(b + align_up(sizeof(float) * (size_t)batch * (size_t)p->n_samples));
   CK(launch_composite(traces, pl, w.y, w.status, s));
-  CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksMajor, s));
+  if (is_pow2(pl.N)) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksMajor, s));
+  else CK(launch_spectrum_band(pl, w.y, w.status, w, nullptr, kPeaksMajor, s));
   return GPOEO_OK;
 }
 
@@ -449,8 +459,7 @@ size_t gpoeo_similarity_workspace_size(int64_t n_queries) {
 int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples, const int32_t* trace_index,
                            const int32_t* period, int64_t n_queries, int32_t num_groups, int32_t gmm_max_iters,
                            double* error_out, void* workspace, size_t workspace_bytes, void* stream) {
-  if (!is_pow2(n_samples) || n_samples < (1 << GPOEO_MIN_LOG2N) || n_samples > (1 << GPOEO_MAX_LOG2N))
-    return GPOEO_ERR_UNSUPPORTED;
+  if (n_samples < (1 << GPOEO_MIN_LOG2N) || n_samples > (1 << GPOEO_MAX_LOG2N)) return GPOEO_ERR_UNSUPPORTED;
   if (batch < 0 || n_queries < 0 || num_groups < 1 || num_groups > GPOEO_MAX_GROUPS || gmm_max_iters < 1)
     return GPOEO_ERR_INVALID_ARGUMENT;
   if (n_queries > 0 && (!signal || !trace_index || !period || !error_out)) return GPOEO_ERR_INVALID_ARGUMENT;
@@ -502,7 +511,8 @@ const char* gpoeo_status_string(int status) {
   switch (status) {
     case GPOEO_OK: return "ok";
     case GPOEO_ERR_INVALID_ARGUMENT: return "invalid argument";
-    case GPOEO_ERR_UNSUPPORTED: return "unsupported (n_samples must be a power of two in [2^3, 2^18])";
+    case GPOEO_ERR_UNSUPPORTED:
+      return "unsupported (n_samples outside [2^3, 2^18], or a non-power-of-two n_samples whose band is too wide)";
     case GPOEO_ERR_WORKSPACE: return "workspace missing or too small";
     case GPOEO_ERR_MISALIGNED: return "misaligned pointer or stride";
     case GPOEO_ERR_CUDA: return "CUDA error (no device or launch failure)";

@@ -130,6 +130,10 @@ enum PeakMode { kPeaksNone = 0, kPeaksCandidates = 1, kPeaksMajor = 2 };
 cudaError_t launch_composite(const float* x, const Plan& p, float* y, int32_t* status, cudaStream_t s);
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
                             int mode, cudaStream_t s);
+// Non-power-of-two N: rows a2 + a3 by the band-limited DFT definition (spectrum.cu).
+size_t band_smem_bytes(const Plan& p, bool all_bins);
+cudaError_t launch_spectrum_band(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
+                                 int mode, cudaStream_t s);
 // Fused a1 + a2 + a3 (N = 65536 only): composite, spectrum and candidates in one kernel.
 // y_out may be null (spectral-only: nothing but the results leaves the chip).
 cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* y_out, float* spectra,

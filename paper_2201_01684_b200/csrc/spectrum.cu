@@ -161,8 +161,8 @@ struct PView {
 // the top K by (P desc, k asc), map k -> floor(N/k) and dedupe (Alg.1 l.3-5, P:311-314;
 // Z5, Z7-Z9); append one Alg. 2 query per candidate and write the trace status. Called
 // by the whole CTA (T threads) that owns ps; Pv sees the whole spectrum.
-template <int C, int T>
-__device__ void finish_candidates(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps,
+template <class PV, int T>
+__device__ void finish_candidates(const Plan& p, const PV& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps,
                                   float pmax) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = T / 32;
@@ -264,8 +264,8 @@ __device__ void finish_candidates(const Plan& p, const PView<C>& Pv, int64_t t, 
 
 // Rows a3 on one CTA: P_max over the in-band peaks, collect the peaks above the
 // threshold, then finish_candidates. Called by the whole CTA of cluster rank 0.
-template <int C, int T>
-__device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps) {
+template <class PV, int T>
+__device__ void find_candidates(const Plan& p, const PV& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = T / 32;
   float best = -1.f;
@@ -292,13 +292,13 @@ __device__ void find_candidates(const Plan& p, const PView<C>& Pv, int64_t t, in
       }
     }
   }
-  finish_candidates<C, T>(p, Pv, t, st, w, ps, pmax);
+  finish_candidates<PV, T>(p, Pv, t, st, w, ps, pmax);
 }
 
 // Spectral-only detector (reading R3): the in-band peak with the largest P, ties
 // to the smaller k, -> period floor(N/k). Called by the whole CTA of cluster rank 0.
-template <int C, int T>
-__device__ void find_major(const Plan& p, const PView<C>& Pv, int64_t t, int32_t st, gpoeo_major_result* out,
+template <class PV, int T>
+__device__ void find_major(const Plan& p, const PV& Pv, int64_t t, int32_t st, gpoeo_major_result* out,
                            PeakShared& ps) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = T / 32;
@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
     } else {
       Pv.base[0] = P;
     }
-    if (mode == kPeaksMajor) find_major<C, T>(p, Pv, t, status_in[t], w.major, ps);
-    else find_candidates<C, T>(p, Pv, t, status_in[t], w, ps);
+    if (mode == kPeaksMajor) find_major<PView<C>, T>(p, Pv, t, status_in[t], w.major, ps);
+    else find_candidates<PView<C>, T>(p, Pv, t, status_in[t], w, ps);
   }
   if constexpr (C > 1) cg::this_cluster().sync();  // keep our P alive while rank 0 reads it
 }
@@ -860,7 +860,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
           Pv.n = kn;
           Pv.base[0] = P;
           Pv.base[1] = Pp;
-          finish_candidates<2, kT>(p, Pv, t, st, w, fs.ps, pmax);
+          finish_candidates<PView<2>, kT>(p, Pv, t, st, w, fs.ps, pmax);
         }
       }
     }
@@ -903,6 +903,114 @@ cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* 
     case 3: return launch_fused_65536<3>(p, x, w, y_out, spectra, mode, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+
+// ===================================================================================
+// Rows a2 + a3 for N that is not a power of two: the power spectrum is evaluated by the
+// DFT definition only at the bins the peak rule reads (the band [k_lo, k_hi] and its two
+// neighbours; every bin 0..N/2 for the debug surface). One CTA per trace; a thread per bin
+// accumulates X_k = sum_n y[n] W_N^(kn) over y staged in shared-memory tiles, the twiddle
+// advanced by a complex product and re-seeded every 64 samples from the exactly reduced
+// angle 2 pi ((k n) mod N) / N. Cost O(N x bins): meant for the moderate, arbitrary lengths
+// of recorded traces and of Alg. 3's suffixes, not for the power-of-two batch path.
+constexpr int kBandT = 256, kBandTile = 2048;
+
+// P[k] held for k in [k0, k0 + nb); mirrored edges (Z5): P[-k] = P[k], P[N - k] = P[k]
+struct BandView {
+  const float* P;
+  int32_t k0, N;
+  __device__ __forceinline__ float operator()(int64_t k) const {
+    if (k < 0) k = -k;
+    if (k > N / 2) k = N - k;
+    return P[k - k0];
+  }
+};
+
+__global__ void __launch_bounds__(kBandT) spectrum_band_kernel(Plan p, const float* __restrict__ y,
+                                                               const int32_t* __restrict__ status_in, Work w,
+                                                               float* __restrict__ spectra, int mode, int kb0,
+                                                               int kb1) {
+  extern __shared__ __align__(16) float sband[];
+  __shared__ PeakShared ps;
+  const int nb = kb1 - kb0 + 1;
+  float* Pb = sband;
+  float* tile = sband + ((nb + 3) & ~3);
+  const int64_t t = blockIdx.x;
+  const int N = p.N;
+  const float* yt = y + t * (int64_t)N;
+  for (int kc = kb0; kc <= kb1; kc += kBandT) {
+    const int k = kc + threadIdx.x;
+    const bool act = k <= kb1;
+    float wr = 1.f, wi = 0.f;
+    if (act) sincospif(-2.0f * (float)k / (float)N, &wi, &wr);
+    float xr = 0.f, xi = 0.f;
+    for (int n0 = 0; n0 < N; n0 += kBandTile) {
+      const int cnt = N - n0 < kBandTile ? N - n0 : kBandTile;
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += kBandT) tile[i] = __ldg(yt + n0 + i);
+      __syncthreads();
+      if (act) {
+        for (int u = 0; u < cnt; u += 64) {
+          const int64_t m = ((int64_t)k * (int64_t)(n0 + u)) % N;
+          float zr, zi;
+          sincospif(-2.0f * (float)m / (float)N, &zi, &zr);
+          const int ve = cnt - u < 64 ? cnt - u : 64;
+          for (int v = 0; v < ve; ++v) {
+            const float yv = tile[u + v];
+            xr = fmaf(yv, zr, xr);
+            xi = fmaf(yv, zi, xi);
+            const float tr = zr * wr - zi * wi;
+            zi = zr * wi + zi * wr;
+            zr = tr;
+          }
+        }
+      }
+    }
+    if (act) {
+      const float pk = xr * xr + xi * xi;
+      Pb[k - kb0] = pk;
+      if (spectra) spectra[t * (int64_t)(N / 2 + 1) + k] = pk;
+    }
+  }
+  __syncthreads();
+  if (mode == kPeaksNone) return;
+  BandView Pv;
+  Pv.P = Pb;
+  Pv.k0 = kb0;
+  Pv.N = N;
+  if (mode == kPeaksMajor) find_major<BandView, kBandT>(p, Pv, t, status_in[t], w.major, ps);
+  else find_candidates<BandView, kBandT>(p, Pv, t, status_in[t], w, ps);
+}
+
+// bins the band kernel evaluates: the band and its two neighbours, or all of 0..N/2
+static void band_bins(const Plan& p, bool all, int* kb0, int* kb1) {
+  const int n = p.N / 2;
+  if (all || p.k_lo > p.k_hi) {
+    *kb0 = 0;
+    *kb1 = n;
+    return;
+  }
+  *kb0 = p.k_lo - 1 < 0 ? 0 : p.k_lo - 1;
+  *kb1 = p.k_hi + 1 > n ? n : p.k_hi + 1;
+}
+
+size_t band_smem_bytes(const Plan& p, bool all) {
+  int kb0, kb1;
+  band_bins(p, all, &kb0, &kb1);
+  return (size_t)(((kb1 - kb0 + 1) + 3) & ~3) * sizeof(float) + (size_t)kBandTile * sizeof(float);
+}
+
+cudaError_t launch_spectrum_band(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
+                                 int mode, cudaStream_t s) {
+  if (p.batch == 0) return cudaSuccess;
+  int kb0, kb1;
+  band_bins(p, spectra != nullptr, &kb0, &kb1);
+  const size_t smem = band_smem_bytes(p, spectra != nullptr);
+  cudaError_t e = cudaFuncSetAttribute(spectrum_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  spectrum_band_kernel<<<(unsigned)p.batch, kBandT, smem, s>>>(p, y, status_in, w, spectra, mode, kb0, kb1);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_spectrum(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,

@@ -55,7 +55,7 @@ def test_default_params_and_struct_layout():
 
 
 @pytest.mark.parametrize("field,value,code", [
-    ("n_samples", 1000, -2), ("n_samples", 4, -2), ("n_samples", 1 << 19, -2),
+    ("n_samples", 4, -2), ("n_samples", 1 << 19, -2),
     ("n_features", 0, -1), ("n_features", 9, -1),
     ("min_period", 1, -1), ("max_period", 513, -1), ("c_peak", 0.0, -1), ("c_peak", 1.5, -1),
     ("max_candidates", 0, -1), ("max_candidates", 33, -1), ("num_groups", 0, -1), ("num_groups", 9, -1),
@@ -66,6 +66,18 @@ def test_validation_codes(field, value, code):
     setattr(p, field, value)
     assert g.validate(p) == code
     assert g.workspace_size(p, 10) == 0
+
+
+def test_non_power_of_two_lengths():
+    # any N in [8, 2^18] (band-limited DFT when N is not a power of two) ...
+    for N in (8, 9, 1000, 4095, 10_001):
+        p = g.default_params(N, 3)
+        assert g.validate(p) == 0 and g.workspace_size(p, 4) > 0
+    # ... unless its band does not fit in shared memory (N/2 bins here)
+    assert g.validate(g.default_params(200_000, 1)) == -2
+    p = g.default_params(200_000, 1)
+    p.min_period = 100  # band k <= 2000: fine
+    assert g.validate(p) == 0
 
 
 def test_workspace_size_monotone():
@@ -81,7 +93,7 @@ def test_errors_are_synchronous_without_a_device():
     p = g.default_params(1024, 1)
     res = ctypes.create_string_buffer(64)
     # invalid argument -> reported before any device work
-    bad = g.default_params(1000, 1)
+    bad = g.default_params(1 << 19, 1)  # N above 2^18
     assert lib.gpoeo_detect_periods(ctypes.c_void_p(16), 1, ctypes.byref(bad), res, ctypes.c_void_p(256), 1 << 20,
                                     None) == -2
     assert lib.gpoeo_detect_periods(ctypes.c_void_p(16), 1, ctypes.byref(p), res, None, 0, None) == -3

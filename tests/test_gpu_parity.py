@@ -23,8 +23,14 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not torch.cuda.is_available(),
 
 
 def _to_dev(x: np.ndarray):
+    """[B][F][N] -> device rows of trace_stride = F*N rounded up to 4 floats (the ABI's
+    16-byte alignment rule; default_params uses the same stride)."""
     B = x.shape[0]
-    return torch.from_numpy(np.ascontiguousarray(x.reshape(B, -1))).cuda()
+    flat = x.reshape(B, -1)
+    stride = (flat.shape[1] + 3) & ~3
+    rows = np.zeros((B, stride), np.float32)
+    rows[:, :flat.shape[1]] = flat
+    return torch.from_numpy(rows).cuda()
 
 
 def _detect(x: np.ndarray, p):
@@ -428,3 +434,30 @@ def test_major_statuses():
     r = g.major_numpy(res)
     assert list(r["status"]) == [O.TRACE_CONSTANT, O.TRACE_APERIODIC, O.TRACE_OK]
     assert r["bin"][2] == 100 and r["period"][2] == N // 100
+
+
+# ---- N not a power of two (band-limited DFT path) -------------------------------------
+
+@pytest.mark.parametrize("N", [999, 1000, 3001, 6000])
+def test_non_pow2_spectrum_matches_oracle(N):
+    spec = tg.CFG2.with_(batch=2, n_samples=N, period_lo=15.0, period_hi=N / 4, min_period=2, max_period=N // 2)
+    x = tg.generate_host(spec)
+    p = g.params_for(spec)
+    spec_d, sig = g.power_spectrum(_to_dev(x), p)
+    spec_d, sig = spec_d.cpu().numpy(), sig.cpu().numpy()
+    for b in range(2):
+        y, _, _, _ = O.composite(x[b])
+        assert (sig[b].view(np.int32) == y.view(np.int32)).all()
+        ref = O.power_spectrum(y)
+        assert np.abs(spec_d[b] - ref).max() <= 1e-4 * ref.max()
+
+
+@pytest.mark.parametrize("N,F", [(1000, 3), (2999, 1), (5000, 3)])
+def test_non_pow2_detect_matches_oracle(N, F):
+    spec = tg.CFG2.with_(batch=12, n_samples=N, n_features=F, period_lo=20.0, period_hi=N / 6, min_period=10,
+                         max_period=N // 3)
+    x = tg.generate_host(spec)
+    res, det, _ = _detect(x, g.params_for(spec))
+    ods = O.detect_batch(x, O.params_for(spec))
+    _compare(res, det, ods, f"N{N}")
+    _major_compare(x, spec, f"major-N{N}")
