@@ -195,6 +195,48 @@ size_t gpoeo_major_workspace_size(const gpoeo_params* p, int64_t batch);
 int gpoeo_detect_major_periods(const float* traces, int64_t batch, const gpoeo_params* p,
                                gpoeo_major_result* results, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Alg. 3 rolling detector on recorded traces ---------------------
+ * The online robust period detection framework applied to a recorded trace,
+ * reading R5: T_init = Alg. 1 on the whole trace; if SmpDur = (N-1) T_s <
+ * c_measure T_init the call ends (lines 3-6); otherwise Alg. 1 runs on every rolling
+ * suffix of the composite signal starting at t_start = max(0, SmpDur - (2 + c_eval step)
+ * T_init) and advancing by step T_init while (SmpDur - t_start)/T_init >= c_measure
+ * (lines 7-13); T_iter is the suffix period with the smallest Err (lines 14-15), Diff the
+ * spread of the suffix periods, SmpDur_next = -1 when Diff < Diff_threshold (stop sampling),
+ * else ceil(SmpDur/max T) max T - SmpDur (lines 16-21). Times in samples internally;
+ * T_s scales the seconds only (Z25). */
+typedef struct {
+  double c_measure;      /* 2                                                      */
+  double step;           /* 0.5                                                    */
+  double c_eval;         /* 6.5                                                    */
+  double diff_threshold; /* 0.05 (not given in the paper)                           */
+} gpoeo_rolling_params;
+
+typedef struct {
+  int32_t status;        /* Alg. 1 status on the whole trace (no rolling unless OK)        */
+  int32_t t_init;        /* T_init in samples (-1 if none)                                 */
+  int32_t t_iter;        /* T_iter in samples (-1 if none)                                 */
+  int32_t n_sub;         /* rolling suffixes evaluated                                     */
+  int32_t early;         /* 1: lines 3-6 ended the call (too short to roll)                */
+  float diff;            /* Diff (lines 16); +inf if no suffix found a period              */
+  float smpdur_next_s;   /* SmpDur_next [s]; -1 = stop sampling                            */
+  float err_iter;        /* Err of the chosen period                                       */
+} gpoeo_rolling_result;  /* 32 bytes */
+
+void gpoeo_default_rolling_params(gpoeo_rolling_params* rp);
+
+/* Workspace bytes for gpoeo_detect_rolling (HOST, pure; 0 if invalid): Alg. 1's workspace
+ * for the batch, the suffix plan and outcomes, and the scratch of one equal-length suffix
+ * group (at most `batch` suffixes of at most N samples). */
+size_t gpoeo_workspace_size_rolling(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t batch);
+
+/* Alg. 3 over a batch of recorded traces (device pointers as gpoeo_detect_periods; results
+ * [batch] device). Suffixes of equal length from all traces are scored in one Alg. 1 call;
+ * the suffix plan needs T_init on the host, so this entry point SYNCHRONISES `stream`
+ * (once in the middle and before returning). */
+int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
+                         gpoeo_rolling_result* results, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Work counters of the last device-pointer call that used `workspace` (HOST read after
  * the caller synchronised): number of Alg.2 queries and CEM sample-passes. Used by
  * bench.py to report ALU roofline numbers. Returns GPOEO_OK. */

@@ -48,8 +48,16 @@ DETAIL_DTYPE = np.dtype([("n_candidates", "<i4"), ("best_bin", "<i4"), ("local_l
                          ("cand_k", "<i4", (MAX_CANDIDATES,)), ("cand_L", "<i4", (MAX_CANDIDATES,)),
                          ("cand_P", "<f4", (MAX_CANDIDATES,)), ("cand_err", "<f8", (MAX_CANDIDATES,)),
                          ("best_err", "<f8")])
+ROLLING_DTYPE = np.dtype([("status", "<i4"), ("t_init", "<i4"), ("t_iter", "<i4"), ("n_sub", "<i4"),
+                          ("early", "<i4"), ("diff", "<f4"), ("smpdur_next_s", "<f4"), ("err_iter", "<f4")])
 MAJOR_DTYPE = np.dtype([("period", "<i4"), ("period_s", "<f4"), ("bin", "<i4"), ("status", "<i4")])
 assert RESULT_DTYPE.itemsize == 24 and DETAIL_DTYPE.itemsize == 664 and MAJOR_DTYPE.itemsize == 16
+assert ROLLING_DTYPE.itemsize == 32
+
+
+class GpoeoRollingParams(ctypes.Structure):
+    _fields_ = [("c_measure", ctypes.c_double), ("step", ctypes.c_double), ("c_eval", ctypes.c_double),
+                ("diff_threshold", ctypes.c_double)]
 
 _lib = None
 
@@ -103,6 +111,13 @@ def load():
     lib.gpoeo_major_workspace_size.restype = ctypes.c_size_t
     lib.gpoeo_detect_major_periods.argtypes = [P, ctypes.c_int64, PP, P, P, ctypes.c_size_t, P]
     lib.gpoeo_detect_major_periods.restype = ctypes.c_int
+    RP = ctypes.POINTER(GpoeoRollingParams)
+    lib.gpoeo_default_rolling_params.argtypes = [RP]
+    lib.gpoeo_default_rolling_params.restype = None
+    lib.gpoeo_workspace_size_rolling.argtypes = [PP, RP, ctypes.c_int64]
+    lib.gpoeo_workspace_size_rolling.restype = ctypes.c_size_t
+    lib.gpoeo_detect_rolling.argtypes = [P, ctypes.c_int64, PP, RP, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_detect_rolling.restype = ctypes.c_int
     lib.gpoeo_read_counters.argtypes = [P, PP, ctypes.c_int64, ctypes.POINTER(GpoeoCounters), P]
     lib.gpoeo_read_counters.restype = ctypes.c_int
     lib.gpoeo_status_string.argtypes = [ctypes.c_int]
@@ -294,6 +309,35 @@ def detect_major_periods(traces, p: GpoeoParams, workspace=None, results=None, s
 
 def major_numpy(results) -> np.ndarray:
     return results.cpu().numpy().view(MAJOR_DTYPE)
+
+
+def default_rolling_params(**kw) -> GpoeoRollingParams:
+    rp = GpoeoRollingParams()
+    load().gpoeo_default_rolling_params(ctypes.byref(rp))
+    for k, v in kw.items():
+        setattr(rp, k, v)
+    return rp
+
+
+def detect_rolling(traces, p: GpoeoParams, rp: GpoeoRollingParams | None = None, stream=None) -> np.ndarray:
+    """Alg. 3 (reading R5) on a CUDA float32 tensor of recorded traces
+    [B][trace_stride]; synchronous; returns ROLLING_DTYPE records on the host."""
+    import torch
+    assert traces.is_cuda and traces.dtype == torch.float32 and traces.is_contiguous()
+    B = traces.shape[0]
+    lib = load()
+    rp = rp or default_rolling_params()
+    need = int(lib.gpoeo_workspace_size_rolling(ctypes.byref(p), ctypes.byref(rp), B))
+    if need == 0:
+        _check(validate(p), "params")
+        raise GpoeoError("invalid rolling parameters")
+    ws = alloc_workspace(need, traces.device)
+    out = torch.empty(B * ROLLING_DTYPE.itemsize, dtype=torch.uint8, device=traces.device)
+    rc = lib.gpoeo_detect_rolling(ctypes.c_void_p(traces.data_ptr()), B, ctypes.byref(p), ctypes.byref(rp),
+                                  ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                  _stream_handle(stream))
+    _check(rc, "gpoeo_detect_rolling")
+    return out.cpu().numpy().view(ROLLING_DTYPE)
 
 
 def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:

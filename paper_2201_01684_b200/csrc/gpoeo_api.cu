@@ -6,8 +6,12 @@
 //   memset(counters) -> composite (a1) -> spectrum+peaks (a2, a3; appends candidate
 //   queries) -> score(candidate queries) (a4) -> select (a5, a6; appends local queries)
 //   -> score(local queries) (a4) -> final (a7).
+#include <math.h>
 #include <stdio.h>
 #include <string.h>
+
+#include <map>
+#include <vector>
 
 #include "gpoeo_internal.cuh"
 
@@ -215,6 +219,66 @@ __global__ void pack_items_kernel(const int32_t* __restrict__ ti, const int32_t*
                                   ItemList list) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) append_item(list, ti[i], per[i], (int)i);
+}
+
+
+// ---- Alg. 3 rolling detector (reading R5) -----------------------------
+static int validate_rolling(const gpoeo_rolling_params* rp) {
+  if (!rp) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (!(rp->c_measure > 0.0) || !(rp->step > 0.0) || !(rp->c_eval >= 0.0) || !(rp->diff_threshold >= 0.0))
+    return GPOEO_ERR_INVALID_ARGUMENT;
+  return GPOEO_OK;
+}
+
+// suffixes per trace: (2 + c_eval step - c_measure) / step + 1 iterations of lines 8-13
+static int64_t rolling_max_sub(const gpoeo_rolling_params* rp) {
+  const double span = (2.0 + rp->c_eval * rp->step) - rp->c_measure;
+  const double j = span < 0.0 ? 0.0 : floor(span / rp->step) + 2.0;
+  return j > 64.0 ? 64 : (int64_t)j;
+}
+
+// parameters of Alg. 1 on a suffix of length Nj (a one-channel sequence, L_max <= Nj/2)
+static gpoeo_params suffix_params(const gpoeo_params* p, int32_t Nj) {
+  gpoeo_params q = *p;
+  q.n_samples = Nj;
+  q.n_features = 1;
+  q.trace_stride = ((int64_t)Nj + 3) & ~(int64_t)3;
+  if (q.max_period > Nj / 2) q.max_period = Nj / 2;
+  for (int c = 0; c < GPOEO_MAX_FEATURES; ++c) q.feature_weights[c] = 1.0f;
+  return q;
+}
+
+struct RollLayout {
+  size_t main, whole, plan, segs, gtrace, gstart, gseg, gsig, gres, gdet, gws, total;
+  int64_t max_sub;
+};
+
+static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t B) {
+  RollLayout R;
+  R.max_sub = rolling_max_sub(rp);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  R.main = take(layout(make_plan(p, B)).total);
+  R.whole = take(sizeof(gpoeo_result) * (size_t)B);
+  R.plan = take(sizeof(RollTrace) * (size_t)B);
+  R.segs = take(sizeof(RollSeg) * (size_t)B * (size_t)R.max_sub);
+  R.gtrace = take(sizeof(int32_t) * (size_t)B);
+  R.gstart = take(sizeof(int32_t) * (size_t)B);
+  R.gseg = take(sizeof(int32_t) * (size_t)B);
+  R.gsig = take(sizeof(float) * (size_t)B * (size_t)((p->n_samples + 3) & ~3));
+  R.gres = take(sizeof(gpoeo_result) * (size_t)B);
+  R.gdet = take(sizeof(gpoeo_detail) * (size_t)B);
+  // one suffix group: at most B suffixes of at most N samples; local ranges bounded by the band
+  gpoeo_params q = suffix_params(p, p->n_samples);
+  Plan pl = make_plan(&q, B);
+  pl.max_local = (int64_t)q.max_period - q.min_period + 1;
+  R.gws = take(layout(pl).total);
+  R.total = o;
+  return R;
 }
 
 }  // namespace
@@ -444,6 +508,119 @@ int gpoeo_detect_major_periods(const float* traces, int64_t batch, const gpoeo_p
   CK(launch_composite(traces, pl, w.y, w.status, s));
   if (is_pow2(pl.N)) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksMajor, s));
   else CK(launch_spectrum_band(pl, w.y, w.status, w, nullptr, kPeaksMajor, s));
+  return GPOEO_OK;
+}
+
+
+void gpoeo_default_rolling_params(gpoeo_rolling_params* rp) {
+  if (!rp) return;
+  rp->c_measure = 2.0;
+  rp->step = 0.5;
+  rp->c_eval = 6.5;
+  rp->diff_threshold = 0.05;
+}
+
+size_t gpoeo_workspace_size_rolling(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t batch) {
+  if (validate(p) != GPOEO_OK || validate_rolling(rp) != GPOEO_OK || batch < 0) return 0;
+  return rolling_layout(p, rp, batch).total;
+}
+
+int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
+                         gpoeo_rolling_result* results, void* workspace, size_t workspace_bytes, void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  v = validate_rolling(rp);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0 || batch >= (1ll << 31)) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!traces || !results)) return GPOEO_ERR_INVALID_ARGUMENT;
+  const RollLayout R = rolling_layout(p, rp, batch);
+  if (!workspace || workspace_bytes < R.total) return GPOEO_ERR_WORKSPACE;
+  if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  if (batch == 0) return GPOEO_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  char* b = static_cast<char*>(workspace);
+  // line 1: T_init = Alg. 1 on every whole trace (the composite y stays in the workspace)
+  const Plan pm = make_plan(p, batch);
+  const Layout Lm = layout(pm);
+  gpoeo_result* whole = reinterpret_cast<gpoeo_result*>(b + R.whole);
+  int rc = run_detect(traces, pm, Lm, b + R.main, whole, nullptr, s);
+  if (rc != GPOEO_OK) return rc;
+  const float* y = carve(pm, Lm, b + R.main).y;
+  std::vector<gpoeo_result> hw((size_t)batch);
+  CK(cudaMemcpyAsync(hw.data(), whole, sizeof(gpoeo_result) * (size_t)batch, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // lines 2-13 on the host (exact sample arithmetic, as the oracle): the suffix plan
+  const int32_t N = p->n_samples;
+  const double smpdur = (double)(N - 1);
+  std::vector<RollTrace> plan((size_t)batch);
+  std::map<int32_t, std::vector<int32_t>> groups;  // suffix length -> suffix indices
+  std::vector<int32_t> sfx_trace, sfx_start;
+  for (int64_t t = 0; t < batch; ++t) {
+    RollTrace& pt = plan[(size_t)t];
+    pt.first = (int32_t)sfx_trace.size();
+    pt.n_sub = 0;
+    pt.early = 0;
+    pt.pad = 0;
+    if (hw[(size_t)t].status != GPOEO_TRACE_OK) continue;
+    const double L0 = (double)hw[(size_t)t].period;
+    if (smpdur < rp->c_measure * L0) {
+      pt.early = 1;
+      continue;
+    }
+    double ts = smpdur - (2.0 + rp->c_eval * rp->step) * L0;
+    if (ts < 0.0) ts = 0.0;
+    while ((smpdur - ts) / L0 >= rp->c_measure && pt.n_sub < R.max_sub) {
+      const int32_t s0 = (int32_t)floor(ts);
+      groups[N - s0].push_back((int32_t)sfx_trace.size());
+      sfx_trace.push_back((int32_t)t);
+      sfx_start.push_back(s0);
+      ++pt.n_sub;
+      ts += rp->step * L0;
+    }
+  }
+  RollTrace* dplan = reinterpret_cast<RollTrace*>(b + R.plan);
+  RollSeg* dsegs = reinterpret_cast<RollSeg*>(b + R.segs);
+  CK(cudaMemcpyAsync(dplan, plan.data(), sizeof(RollTrace) * (size_t)batch, cudaMemcpyHostToDevice, s));
+  if (!sfx_trace.empty())
+    CK(cudaMemsetAsync(dsegs, 0xFF, sizeof(RollSeg) * sfx_trace.size(), s));  // period -1: none
+  // Alg. 1 on every suffix, equal lengths in one call (line 11)
+  int32_t* gtrace = reinterpret_cast<int32_t*>(b + R.gtrace);
+  int32_t* gstart = reinterpret_cast<int32_t*>(b + R.gstart);
+  int32_t* gseg = reinterpret_cast<int32_t*>(b + R.gseg);
+  float* gsig = reinterpret_cast<float*>(b + R.gsig);
+  gpoeo_result* gres = reinterpret_cast<gpoeo_result*>(b + R.gres);
+  gpoeo_detail* gdet = reinterpret_cast<gpoeo_detail*>(b + R.gdet);
+  std::vector<int32_t> ht, hs;
+  for (const auto& kv : groups) {
+    const int32_t Nj = kv.first;
+    const std::vector<int32_t>& idx = kv.second;
+    const gpoeo_params q = suffix_params(p, Nj);
+    if (validate(&q) != GPOEO_OK) continue;  // e.g. L_min > Nj/2: no period (as the oracle)
+    const int32_t n = (int32_t)idx.size();
+    ht.resize(n);
+    hs.resize(n);
+    for (int32_t r = 0; r < n; ++r) {
+      ht[r] = sfx_trace[idx[r]];
+      hs[r] = sfx_start[idx[r]];
+    }
+    CK(cudaMemcpyAsync(gtrace, ht.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(gstart, hs.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(gseg, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(launch_gather_suffix(y, N, gtrace, gstart, n, Nj, q.trace_stride, gsig, s));
+    const Plan pq = make_plan(&q, n);
+    const Layout Lq = layout(pq);
+    if (Lq.total > R.total - R.gws) return GPOEO_ERR_WORKSPACE;  // not expected: R.gws bounds it
+    rc = run_detect(gsig, pq, Lq, b + R.gws, gres, gdet, s);
+    if (rc != GPOEO_OK) return rc;
+    CK(launch_scatter_suffix(gres, gdet, n, gseg, dsegs, s));
+    // the host index vectors are reused by the next group: pageable H2D copies are staged
+    // before cudaMemcpyAsync returns, so rewriting them is safe
+  }
+  // lines 14-21
+  RollParamsDev rpd{rp->c_measure, rp->step, rp->c_eval, rp->diff_threshold};
+  CK(launch_rolling_final(batch, N, p->sample_interval, rpd, whole, dplan, dsegs, results, s));
+  CK(cudaStreamSynchronize(s));
   return GPOEO_OK;
 }
 

@@ -141,6 +141,29 @@ cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* 
 cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
                          int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);
+
+// Alg. 3 (rolling.cu): per-suffix outcome, per-trace suffix plan, parameters
+struct RollSeg {
+  int32_t status;
+  int32_t period;  // -1: no period
+  double err;      // Err(L*) of Alg. 1 on the suffix, fp64
+};
+struct RollTrace {
+  int32_t first;   // index of the trace's first suffix in the RollSeg array
+  int32_t n_sub;   // suffixes evaluated (lines 8-13)
+  int32_t early;   // lines 3-6 ended the call
+  int32_t pad;
+};
+struct RollParamsDev {
+  double c_measure, step, c_eval, diff_threshold;
+};
+cudaError_t launch_gather_suffix(const float* y, int32_t N, const int32_t* trace, const int32_t* start, int32_t n,
+                                 int32_t len, int64_t stride, float* dst, cudaStream_t s);
+cudaError_t launch_scatter_suffix(const gpoeo_result* res, const gpoeo_detail* det, int32_t n, const int32_t* seg,
+                                  RollSeg* out, cudaStream_t s);
+cudaError_t launch_rolling_final(int64_t batch, int32_t N, double Ts, RollParamsDev rp, const gpoeo_result* whole,
+                                 const RollTrace* plan, const RollSeg* segs, gpoeo_rolling_result* out,
+                                 cudaStream_t s);
 cudaError_t launch_final(const Plan& p, Work w, gpoeo_result* results, gpoeo_detail* detail, cudaStream_t s);
 
 

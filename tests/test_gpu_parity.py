@@ -461,3 +461,59 @@ def test_non_pow2_detect_matches_oracle(N, F):
     ods = O.detect_batch(x, O.params_for(spec))
     _compare(res, det, ods, f"N{N}")
     _major_compare(x, spec, f"major-N{N}")
+
+
+# ---- Alg. 3 rolling detector (oracle R1, reading R5) ------------------
+
+def _rolling_compare(x, spec, label):
+    p = g.params_for(spec)
+    r = g.detect_rolling(_to_dev(x), p)
+    op = O.params_for(spec, dft_band_only=True)
+    n_amb = 0
+    for i in range(x.shape[0]):
+        o = O.rolling(x[i], op)
+        assert r[i]["status"] == o.status, (label, i)
+        if o.status != O.TRACE_OK:
+            assert r[i]["t_iter"] == -1
+            continue
+        whole = O.detect(x[i], op)
+        if whole.ambiguous():
+            n_amb += 1
+            continue
+        assert r[i]["t_init"] == o.t_init, (label, i)
+        assert bool(r[i]["early"]) == o.early and r[i]["n_sub"] == len(o.sub_start), (label, i)
+        # the suffix decisions: ambiguous suffixes (Z27) may legitimately differ
+        y = O.composite(x[i])[0]
+        sub_amb = False
+        for s0, T in zip(o.sub_start, o.sub_period):
+            q = O.Params(len(y) - s0, 1, min_period=spec.min_period, max_period=min(spec.max_period, (len(y) - s0) // 2),
+                         dft_band_only=True)
+            if q.min_period <= q.max_period and O.detect(y[s0:][None], q).ambiguous():
+                sub_amb = True
+        if sub_amb:
+            n_amb += 1
+            continue
+        assert r[i]["t_iter"] == o.t_iter, (label, i, r[i]["t_iter"], o.t_iter, o.sub_period)
+        want_next = np.float32(o.smpdur_next * 1.0) if o.smpdur_next >= 0 else np.float32(-1.0)
+        assert r[i]["smpdur_next_s"] == want_next, (label, i, r[i]["smpdur_next_s"], o.smpdur_next)
+        if np.isfinite(o.diff):
+            assert abs(r[i]["diff"] - o.diff) <= 1e-6 * max(1.0, o.diff)
+    assert n_amb <= max(1, x.shape[0] // 5), (label, n_amb)
+
+
+def test_rolling_config1():
+    x = tg.generate_host(tg.CFG1)
+    r = g.detect_rolling(_to_dev(x), g.params_for(tg.CFG1))
+    assert r[0]["t_init"] == 37 and r[0]["t_iter"] == 37 and r[0]["n_sub"] == 7 and r[0]["smpdur_next_s"] == -1.0
+    _rolling_compare(x, tg.CFG1, "cfg1")
+
+
+def test_rolling_config2_slice():
+    spec = tg.CFG2.with_(batch=16)
+    _rolling_compare(tg.generate_host(spec), spec, "cfg2")
+
+
+def test_rolling_period_shift():
+    # mid-trace period change (config 5's structure at N = 8192): the suffixes see the new period
+    spec = tg.CFG5.with_(batch=6, n_samples=8192, period_lo=30.0, period_hi=200.0, max_period=2048)
+    _rolling_compare(tg.generate_host(spec), spec, "shift")
