@@ -226,14 +226,15 @@ typedef struct {
 void gpoeo_default_rolling_params(gpoeo_rolling_params* rp);
 
 /* Workspace bytes for gpoeo_detect_rolling (HOST, pure; 0 if invalid): Alg. 1's workspace
- * for the batch, the suffix plan and outcomes, and the scratch of one equal-length suffix
- * group (at most `batch` suffixes of at most N samples). */
+ * for the batch, the suffix plan and outcomes, and the scratch of one ragged suffix batch
+ * (at most `batch` rows of at most N samples). */
 size_t gpoeo_workspace_size_rolling(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t batch);
 
 /* Alg. 3 over a batch of recorded traces (device pointers as gpoeo_detect_periods; results
- * [batch] device). Suffixes of equal length from all traces are scored in one Alg. 1 call;
- * the suffix plan needs T_init on the host, so this entry point SYNCHRONISES `stream`
- * (once in the middle and before returning). */
+ * [batch] device). The suffixes of all traces run through Alg. 1 as ragged batches of up to
+ * `batch` rows (each row a one-channel sequence of its own length); the suffix plan needs
+ * T_init on the host, so this entry point SYNCHRONISES `stream` (once in the middle and
+ * before returning). */
 int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
                          gpoeo_rolling_result* results, void* workspace, size_t workspace_bytes, void* stream);
 

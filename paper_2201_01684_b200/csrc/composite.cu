@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
                                                                 float* __restrict__ y, int32_t* __restrict__ status) {
   __shared__ double red[kCompThreads / 32];
   const int64_t t = blockIdx.x;
+  if (plan.row_n) N = plan.row_n[t];  // ragged batch: this row's length
   const float* xt = x + t * stride;
   float m[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
   bool all_const = true;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
     if (sigma > 0.0) all_const = false;
   }
   if (threadIdx.x == 0) status[t] = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
-  float* yt = y + t * (int64_t)N;
+  float* yt = y + t * plan.ystride;
   if ((N & 3) == 0) {
 #pragma unroll 4
     for (int i = threadIdx.x; i < N / 4; i += kCompThreads) {

@@ -10,7 +10,6 @@
 #include <stdio.h>
 #include <string.h>
 
-#include <map>
 #include <vector>
 
 #include "gpoeo_internal.cuh"
@@ -81,6 +80,8 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
   for (int c = 0; c < GPOEO_MAX_FEATURES; ++c) pl.w[c] = p->feature_weights[c];
   pl.Ts = p->sample_interval;
   pl.batch = batch;
+  pl.ystride = pl.N;
+  pl.row_n = nullptr;
   // band (Z21): floor(N/k) <= Lmax  <=>  k >= floor(N/(Lmax+1)) + 1;  floor(N/k) >= Lmin <=> k <= floor(N/Lmin)
   int64_t klo = (int64_t)pl.N / ((int64_t)pl.Lmax + 1) + 1;
   int64_t khi = (int64_t)pl.N / pl.Lmin;
@@ -188,12 +189,13 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   Work w = carve(pl, L, ws);
   CK(mark(0));
   CK(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));
-  const bool fused = pl.N == 65536 && pl.F <= 3;  // configs 3/4: one kernel reads x once (spectrum.cu)
+  // configs 3/4: one kernel reads x once (spectrum.cu); ragged rows (Alg. 3) take the band DFT
+  const bool fused = !pl.row_n && pl.N == 65536 && pl.F <= 3;
   if (pl.batch > 0 && !fused) CK(launch_composite(traces, pl, w.y, w.status, s));
   CK(mark(1));
   if (pl.batch > 0) {
     if (fused) CK(launch_spectral_fused(pl, traces, w, w.y, nullptr, kPeaksCandidates, s));
-    else if (is_pow2(pl.N)) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
+    else if (!pl.row_n && is_pow2(pl.N)) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
     else CK(launch_spectrum_band(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
   }
   CK(mark(2));
@@ -249,7 +251,7 @@ static gpoeo_params suffix_params(const gpoeo_params* p, int32_t Nj) {
 }
 
 struct RollLayout {
-  size_t main, whole, plan, segs, gtrace, gstart, gseg, gsig, gres, gdet, gws, total;
+  size_t main, whole, plan, segs, gtrace, gstart, gseg, grown, gsig, gres, gdet, gws, total;
   int64_t max_sub;
 };
 
@@ -269,10 +271,11 @@ static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_para
   R.gtrace = take(sizeof(int32_t) * (size_t)B);
   R.gstart = take(sizeof(int32_t) * (size_t)B);
   R.gseg = take(sizeof(int32_t) * (size_t)B);
+  R.grown = take(sizeof(int32_t) * (size_t)B);
   R.gsig = take(sizeof(float) * (size_t)B * (size_t)((p->n_samples + 3) & ~3));
   R.gres = take(sizeof(gpoeo_result) * (size_t)B);
   R.gdet = take(sizeof(gpoeo_detail) * (size_t)B);
-  // one suffix group: at most B suffixes of at most N samples; local ranges bounded by the band
+  // one chunk of suffixes: at most B rows of at most N samples; local ranges bounded by the band
   gpoeo_params q = suffix_params(p, p->n_samples);
   Plan pl = make_plan(&q, B);
   pl.max_local = (int64_t)q.max_period - q.min_period + 1;
@@ -554,7 +557,6 @@ int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params*
   const int32_t N = p->n_samples;
   const double smpdur = (double)(N - 1);
   std::vector<RollTrace> plan((size_t)batch);
-  std::map<int32_t, std::vector<int32_t>> groups;  // suffix length -> suffix indices
   std::vector<int32_t> sfx_trace, sfx_start;
   for (int64_t t = 0; t < batch; ++t) {
     RollTrace& pt = plan[(size_t)t];
@@ -572,7 +574,6 @@ int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params*
     if (ts < 0.0) ts = 0.0;
     while ((smpdur - ts) / L0 >= rp->c_measure && pt.n_sub < R.max_sub) {
       const int32_t s0 = (int32_t)floor(ts);
-      groups[N - s0].push_back((int32_t)sfx_trace.size());
       sfx_trace.push_back((int32_t)t);
       sfx_start.push_back(s0);
       ++pt.n_sub;
@@ -584,38 +585,53 @@ int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params*
   CK(cudaMemcpyAsync(dplan, plan.data(), sizeof(RollTrace) * (size_t)batch, cudaMemcpyHostToDevice, s));
   if (!sfx_trace.empty())
     CK(cudaMemsetAsync(dsegs, 0xFF, sizeof(RollSeg) * sfx_trace.size(), s));  // period -1: none
-  // Alg. 1 on every suffix, equal lengths in one call (line 11)
+  // Alg. 1 on every suffix (line 11): the suffixes, each a one-channel sequence of its own
+  // length, run as ragged batches of up to `batch` rows (per-row N: Plan::row_n)
   int32_t* gtrace = reinterpret_cast<int32_t*>(b + R.gtrace);
   int32_t* gstart = reinterpret_cast<int32_t*>(b + R.gstart);
   int32_t* gseg = reinterpret_cast<int32_t*>(b + R.gseg);
+  int32_t* grown = reinterpret_cast<int32_t*>(b + R.grown);
   float* gsig = reinterpret_cast<float*>(b + R.gsig);
   gpoeo_result* gres = reinterpret_cast<gpoeo_result*>(b + R.gres);
   gpoeo_detail* gdet = reinterpret_cast<gpoeo_detail*>(b + R.gdet);
-  std::vector<int32_t> ht, hs;
-  for (const auto& kv : groups) {
-    const int32_t Nj = kv.first;
-    const std::vector<int32_t>& idx = kv.second;
-    const gpoeo_params q = suffix_params(p, Nj);
-    if (validate(&q) != GPOEO_OK) continue;  // e.g. L_min > Nj/2: no period (as the oracle)
-    const int32_t n = (int32_t)idx.size();
-    ht.resize(n);
-    hs.resize(n);
-    for (int32_t r = 0; r < n; ++r) {
-      ht[r] = sfx_trace[idx[r]];
-      hs[r] = sfx_start[idx[r]];
+  // suffixes shorter than the smallest supported sequence (8 samples) find no period (the
+  // oracle rejects them too)
+  std::vector<int32_t> run_trace, run_start, run_seg;
+  for (size_t i = 0; i < sfx_trace.size(); ++i)
+    if (N - sfx_start[i] >= (1 << GPOEO_MIN_LOG2N)) {
+      run_trace.push_back(sfx_trace[i]);
+      run_start.push_back(sfx_start[i]);
+      run_seg.push_back((int32_t)i);
     }
-    CK(cudaMemcpyAsync(gtrace, ht.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(gstart, hs.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(gseg, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(launch_gather_suffix(y, N, gtrace, gstart, n, Nj, q.trace_stride, gsig, s));
-    const Plan pq = make_plan(&q, n);
-    const Layout Lq = layout(pq);
-    if (Lq.total > R.total - R.gws) return GPOEO_ERR_WORKSPACE;  // not expected: R.gws bounds it
-    rc = run_detect(gsig, pq, Lq, b + R.gws, gres, gdet, s);
+  const int64_t nrun = (int64_t)run_seg.size();
+  std::vector<int32_t> hn;
+  for (int64_t c0 = 0; c0 < nrun; c0 += batch) {
+    const int32_t n = (int32_t)(nrun - c0 < batch ? nrun - c0 : batch);
+    hn.resize(n);
+    int32_t Smax = 0;
+    for (int32_t r = 0; r < n; ++r) {
+      hn[r] = N - run_start[c0 + r];
+      if (hn[r] > Smax) Smax = hn[r];
+    }
+    const int32_t S = (Smax + 3) & ~3;
+    const gpoeo_params q = suffix_params(p, S);
+    if (q.min_period > q.max_period) continue;  // every row too short for L_min: no period (as the oracle)
+    CK(cudaMemcpyAsync(gtrace, run_trace.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(gstart, run_start.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(grown, hn.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(gseg, run_seg.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(launch_gather_suffix_ragged(y, N, gtrace, gstart, grown, n, S, gsig, s));
+    Plan pr = make_plan(&q, n);
+    pr.row_n = grown;
+    pr.max_local = (int64_t)q.max_period - q.min_period + 1;  // rows clip L_max to N_j/2: bound
+    const Layout Lr = layout(pr);
+    if (Lr.total > R.total - R.gws) return GPOEO_ERR_WORKSPACE;  // not expected: R.gws bounds it
+    if (band_smem_bytes(pr, false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
+    rc = run_detect(gsig, pr, Lr, b + R.gws, gres, gdet, s);
     if (rc != GPOEO_OK) return rc;
     CK(launch_scatter_suffix(gres, gdet, n, gseg, dsegs, s));
-    // the host index vectors are reused by the next group: pageable H2D copies are staged
-    // before cudaMemcpyAsync returns, so rewriting them is safe
+    // the host vectors are rewritten by the next chunk: pageable H2D copies are staged before
+    // cudaMemcpyAsync returns
   }
   // lines 14-21
   RollParamsDev rpd{rp->c_measure, rp->step, rp->c_eval, rp->diff_threshold};
@@ -659,6 +675,7 @@ int gpoeo_similarity_error(const float* signal, int64_t batch, int32_t n_samples
   pl.G = num_groups;
   pl.maxit = gmm_max_iters;
   pl.batch = batch;
+  pl.ystride = n_samples;
   ItemList list{items, n_queries, &ctr[CTR_A_SMALL], &ctr[CTR_A_BIG], &ctr[CTR_CUR_A_SMALL], &ctr[CTR_CUR_A_BIG],
                 xl, &ctr[CTR_A_XL], &ctr[CTR_CUR_A_XL]};
   CK(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * kCounterSlots, s));

@@ -28,7 +28,28 @@ struct Plan {
   double Ts;
   int64_t max_local;          // per-trace upper bound on the local-range size
   int64_t batch;
+  int64_t ystride;            // floats between rows of the composite signal y (N when uniform)
+  const int32_t* row_n;       // ragged batch (Alg. 3 suffixes, F = 1): per-row N, or null
 };
+
+// The plan of row t: a ragged batch carries its own N per row (L_max clipped to N/2, the
+// band recomputed: Z21); otherwise the call's plan.
+__device__ __forceinline__ Plan row_plan(const Plan& p, int64_t t) {
+  Plan r = p;
+  if (p.row_n) {
+    const int32_t N = p.row_n[t];
+    r.N = N;
+    r.n = N / 2;
+    r.Lmax = p.Lmax < N / 2 ? p.Lmax : N / 2;
+    int64_t klo = (int64_t)N / ((int64_t)r.Lmax + 1) + 1;
+    int64_t khi = (int64_t)N / p.Lmin;
+    if (klo < 1) klo = 1;
+    if (khi > r.n) khi = r.n;
+    r.k_lo = (int32_t)klo;
+    r.k_hi = (int32_t)khi;
+  }
+  return r;
+}
 
 enum CounterSlot {
   CTR_A_SMALL = 0,     // candidate queries with L < kBucketMinL (front of items_a)
@@ -157,8 +178,8 @@ struct RollTrace {
 struct RollParamsDev {
   double c_measure, step, c_eval, diff_threshold;
 };
-cudaError_t launch_gather_suffix(const float* y, int32_t N, const int32_t* trace, const int32_t* start, int32_t n,
-                                 int32_t len, int64_t stride, float* dst, cudaStream_t s);
+cudaError_t launch_gather_suffix_ragged(const float* y, int32_t N, const int32_t* trace, const int32_t* start,
+                                        const int32_t* len, int32_t n, int64_t stride, float* dst, cudaStream_t s);
 cudaError_t launch_scatter_suffix(const gpoeo_result* res, const gpoeo_detail* det, int32_t n, const int32_t* seg,
                                   RollSeg* out, cudaStream_t s);
 cudaError_t launch_rolling_final(int64_t batch, int32_t N, double Ts, RollParamsDev rp, const gpoeo_result* whole,

@@ -1,21 +1,22 @@
 // rolling.cu — SURVEY 8f row 1: Alg. 3, the online robust period detection framework
 // (P:383-429), on recorded traces (reading R5). The host entry point
 // (gpoeo_detect_rolling, gpoeo_api.cu) runs Alg. 1 on the whole traces, plans the rolling
-// suffixes of each trace (lines 7-13), runs Alg. 1 on every suffix — suffixes of equal
-// length batched into one call — and these kernels move the suffixes and combine the
-// per-suffix periods (lines 14-21).
+// suffixes of each trace (lines 7-13), runs Alg. 1 on every suffix as ragged batches (each
+// row a one-channel sequence of its own length: Plan::row_n), and these kernels move the
+// suffixes and combine the per-suffix periods (lines 14-21).
 #include "gpoeo_internal.cuh"
 
 namespace gpoeo {
 
-// rows r < n: dst[r][0 .. len) = y[trace[r]][start[r] .. start[r] + len), zero pad to stride
-__global__ void gather_suffix_kernel(const float* __restrict__ y, int32_t N, const int32_t* __restrict__ trace,
-                                     const int32_t* __restrict__ start, int32_t len, int64_t stride,
-                                     float* __restrict__ dst) {
+// ragged rows r < n: dst[r][0 .. len[r]) = y[trace[r]][start[r] ..), zero pad to stride
+__global__ void gather_suffix_ragged_kernel(const float* __restrict__ y, int32_t N, const int32_t* __restrict__ trace,
+                                            const int32_t* __restrict__ start, const int32_t* __restrict__ len,
+                                            int64_t stride, float* __restrict__ dst) {
   const int64_t r = blockIdx.x;
   const float* src = y + (int64_t)trace[r] * N + start[r];
+  const int32_t n = len[r];
   float* d = dst + r * stride;
-  for (int64_t i = threadIdx.x; i < stride; i += blockDim.x) d[i] = i < len ? __ldg(src + i) : 0.f;
+  for (int64_t i = threadIdx.x; i < stride; i += blockDim.x) d[i] = i < n ? __ldg(src + i) : 0.f;
 }
 
 // per-suffix outcome of Alg. 1 (status, L*, Err(L*) in fp64 from the detail record)
@@ -89,10 +90,10 @@ __global__ void rolling_final_kernel(int64_t batch, int32_t N, double Ts, RollPa
   out[t] = r;
 }
 
-cudaError_t launch_gather_suffix(const float* y, int32_t N, const int32_t* trace, const int32_t* start, int32_t n,
-                                 int32_t len, int64_t stride, float* dst, cudaStream_t s) {
+cudaError_t launch_gather_suffix_ragged(const float* y, int32_t N, const int32_t* trace, const int32_t* start,
+                                        const int32_t* len, int32_t n, int64_t stride, float* dst, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  gather_suffix_kernel<<<n, 256, 0, s>>>(y, N, trace, start, len, stride, dst);
+  gather_suffix_ragged_kernel<<<n, 256, 0, s>>>(y, N, trace, start, len, stride, dst);
   return cudaGetLastError();
 }
 

@@ -964,6 +964,8 @@ struct ScoreArgs {
   int reverse;         // 1: item k is items[cap - 1 - k]
   double* err_out;
   uint8_t* lab_scratch;  // [gridDim][warps][lab_stride] streaming path (L > bucket_lcap)
+  const int32_t* row_n;  // ragged batch: per-row N (else null: a.N)
+  int64_t ystride;       // floats between rows of y
   int32_t lab_stride;
   int32_t bucket_lcap;   // bucket path handles kBucketMinL <= L <= bucket_lcap
   unsigned long long* cem_ctr;
@@ -994,8 +996,8 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
     const int4 q = fetch_item(a, item);
     const int64_t t = q.x;
     const int32_t L = q.y;
-    const int32_t npairs = a.N / L - 1;
-    const float* yt = a.y + t * (int64_t)a.N;
+    const int32_t npairs = (a.row_n ? a.row_n[t] : a.N) / L - 1;
+    const float* yt = a.y + t * a.ystride;
     double acc = 0.0;
     int tau = 1;
     while (tau * kLpt < L) tau <<= 1;
@@ -1050,8 +1052,8 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
     const int4 q = fetch_item(a, item);
     const int64_t t = q.x;
     const int32_t L = q.y;
-    const int32_t npairs = a.N / L - 1;
-    const float* yt = a.y + t * (int64_t)a.N;
+    const int32_t npairs = (a.row_n ? a.row_n[t] : a.N) / L - 1;
+    const float* yt = a.y + t * a.ystride;
     double acc = 0.0;
     if (L <= a.bucket_lcap) {
       BucketView bv = BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap), a.bucket_lcap);
@@ -1181,6 +1183,8 @@ cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, do
   ScoreArgs a{};
   a.y = y;
   a.N = p.N;
+  a.row_n = p.row_n;
+  a.ystride = p.ystride;
   a.maxit = p.maxit;
   a.items = list.items;
   a.cap = list.cap;

@@ -13,9 +13,10 @@
 namespace gpoeo {
 
 // One thread per trace: argmin (Err, L) over candidates, local range, work-list append.
-__global__ void select_kernel(Plan p, Work w) {
+__global__ void select_kernel(Plan pc, Work w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= p.batch) return;
+  if (t >= pc.batch) return;
+  const Plan p = row_plan(pc, t);
   if (w.status[t] != GPOEO_TRACE_OK) return;
   const int nc = w.n_cand[t];
   int best = 0;
@@ -55,9 +56,10 @@ __global__ void select_kernel(Plan p, Work w) {
 }
 
 // One thread per trace: argmin (Err, L) over the local range -> result (+ detail).
-__global__ void final_kernel(Plan p, Work w, gpoeo_result* __restrict__ res, gpoeo_detail* __restrict__ det) {
+__global__ void final_kernel(Plan pc, Work w, gpoeo_result* __restrict__ res, gpoeo_detail* __restrict__ det) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= p.batch) return;
+  if (t >= pc.batch) return;
+  const Plan p = row_plan(pc, t);
   const int32_t st = w.status[t];
   gpoeo_result r;
   r.status = st;

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
   const int q = (C > 1) ? (int)(blockIdx.x % C) : 0;
   const int64_t t = blockIdx.x / C;
   const int n = n2 * C;
-  const float2* z = reinterpret_cast<const float2*>(y + t * (int64_t)p.N);
+  const float2* z = reinterpret_cast<const float2*>(y + t * p.ystride);
 
   // ---- load + DIF split across the cluster: a_q[j2] -------------------------------
   for (int j2 = threadIdx.x; j2 < n2; j2 += T) {
@@ -927,18 +927,31 @@ struct BandView {
   }
 };
 
-__global__ void __launch_bounds__(kBandT) spectrum_band_kernel(Plan p, const float* __restrict__ y,
+__device__ __forceinline__ void band_bins_of(const Plan& p, bool all, int* kb0, int* kb1) {
+  const int n = p.N / 2;
+  if (all || p.k_lo > p.k_hi) {
+    *kb0 = 0;
+    *kb1 = n;
+    return;
+  }
+  *kb0 = p.k_lo - 1 < 0 ? 0 : p.k_lo - 1;
+  *kb1 = p.k_hi + 1 > n ? n : p.k_hi + 1;
+}
+
+__global__ void __launch_bounds__(kBandT) spectrum_band_kernel(Plan pc, const float* __restrict__ y,
                                                                const int32_t* __restrict__ status_in, Work w,
-                                                               float* __restrict__ spectra, int mode, int kb0,
-                                                               int kb1) {
+                                                               float* __restrict__ spectra, int mode, int all,
+                                                               int tile_off) {
   extern __shared__ __align__(16) float sband[];
   __shared__ PeakShared ps;
-  const int nb = kb1 - kb0 + 1;
-  float* Pb = sband;
-  float* tile = sband + ((nb + 3) & ~3);
   const int64_t t = blockIdx.x;
+  const Plan p = row_plan(pc, t);  // a ragged row's own N and band
+  int kb0, kb1;
+  band_bins_of(p, all != 0, &kb0, &kb1);
+  float* Pb = sband;
+  float* tile = sband + tile_off;
   const int N = p.N;
-  const float* yt = y + t * (int64_t)N;
+  const float* yt = y + t * pc.ystride;
   for (int kc = kb0; kc <= kb1; kc += kBandT) {
     const int k = kc + threadIdx.x;
     const bool act = k <= kb1;
@@ -983,33 +996,30 @@ __global__ void __launch_bounds__(kBandT) spectrum_band_kernel(Plan p, const flo
   else find_candidates<BandView, kBandT>(p, Pv, t, status_in[t], w, ps);
 }
 
-// bins the band kernel evaluates: the band and its two neighbours, or all of 0..N/2
-static void band_bins(const Plan& p, bool all, int* kb0, int* kb1) {
+// bins the band kernel keeps: the band and its two neighbours, or all of 0..N/2. For a
+// ragged batch p is sized for the longest row: its band (N/L_min) bounds every row's.
+static int band_slots(const Plan& p, bool all) {
   const int n = p.N / 2;
-  if (all || p.k_lo > p.k_hi) {
-    *kb0 = 0;
-    *kb1 = n;
-    return;
-  }
-  *kb0 = p.k_lo - 1 < 0 ? 0 : p.k_lo - 1;
-  *kb1 = p.k_hi + 1 > n ? n : p.k_hi + 1;
+  if (all || p.k_lo > p.k_hi) return n + 1;
+  const int kb0 = p.k_lo - 1 < 0 ? 0 : p.k_lo - 1;
+  const int khi = p.row_n ? p.N / p.Lmin : p.k_hi;  // rows clip L_max to N_j/2: bands may start at 1
+  const int kb1 = khi + 1 > n ? n : khi + 1;
+  return (p.row_n ? kb1 + 1 : kb1 - kb0 + 1);
 }
 
 size_t band_smem_bytes(const Plan& p, bool all) {
-  int kb0, kb1;
-  band_bins(p, all, &kb0, &kb1);
-  return (size_t)(((kb1 - kb0 + 1) + 3) & ~3) * sizeof(float) + (size_t)kBandTile * sizeof(float);
+  return (size_t)((band_slots(p, all) + 3) & ~3) * sizeof(float) + (size_t)kBandTile * sizeof(float);
 }
 
 cudaError_t launch_spectrum_band(const Plan& p, const float* y, const int32_t* status_in, Work w, float* spectra,
                                  int mode, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
-  int kb0, kb1;
-  band_bins(p, spectra != nullptr, &kb0, &kb1);
-  const size_t smem = band_smem_bytes(p, spectra != nullptr);
+  const bool all = spectra != nullptr;
+  const size_t smem = band_smem_bytes(p, all);
   cudaError_t e = cudaFuncSetAttribute(spectrum_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  spectrum_band_kernel<<<(unsigned)p.batch, kBandT, smem, s>>>(p, y, status_in, w, spectra, mode, kb0, kb1);
+  spectrum_band_kernel<<<(unsigned)p.batch, kBandT, smem, s>>>(p, y, status_in, w, spectra, mode, all ? 1 : 0,
+                                                              (band_slots(p, all) + 3) & ~3);
   return cudaGetLastError();
 }
 
