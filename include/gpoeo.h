@@ -238,6 +238,38 @@ size_t gpoeo_workspace_size_rolling(const gpoeo_params* p, const gpoeo_rolling_p
 int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
                          gpoeo_rolling_result* results, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Alg. 4 adaptive feature measurement on simulated telemetry -------
+ * Alg. 4 lines 1-7, reading R6: each trace is the complete recorded
+ * telemetry of one application (the simulated sampling backend: sample n becomes
+ * available at time n T_s). A session starts with init_samples samples (SmpDur_init);
+ * every round runs Alg. 3 (gpoeo_detect_rolling's rule) on each unfinished session's samples
+ * so far and, while SmpDur_next > 0, waits SmpDur_next (appends that many samples) and
+ * repeats; SmpDur_next <= 0 ends the session with T_iter, and the feature measurement of
+ * lines 8-10 is restarted at the current sample for T_iter samples. A session that would
+ * need more samples than the recording holds ends UNSTABLE with its last T_iter. All
+ * unfinished sessions of a round run as one ragged Alg. 3 batch. */
+#define GPOEO_TRACE_UNSTABLE 4 /* Alg. 4: the recording ended before T_iter was stable */
+typedef struct {
+  int32_t status;        /* gpoeo_trace_status of the last Alg. 3 call, or GPOEO_TRACE_UNSTABLE */
+  int32_t t_iter;        /* T_iter in samples (-1 if none)                                  */
+  int32_t rounds;        /* Alg. 3 calls (lines 3-7)                                        */
+  int32_t samples;       /* samples collected when the loop ended                           */
+  int32_t measure_start; /* feature measurement restart (line 8): sample index              */
+  int32_t measure_end;   /* ... stop after T_iter (line 9): measure_start + t_iter           */
+  float t_iter_s;        /* T_iter [s]                                                      */
+  float err_iter;        /* Err of T_iter                                                   */
+} gpoeo_measure_result;  /* 32 bytes */
+
+size_t gpoeo_workspace_size_measure(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t batch);
+
+/* Alg. 4 over `batch` sessions. traces: device [batch][trace_stride], the recordings
+ * (n_samples = the recording length); init_samples: SmpDur_init / T_s + 1, in [8, n_samples];
+ * results: HOST [batch]. SYNCHRONISES `stream` (every round needs the previous one's
+ * SmpDur_next on the host). */
+int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
+                           int32_t init_samples, gpoeo_measure_result* results, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* Work counters of the last device-pointer call that used `workspace` (HOST read after
  * the caller synchronised): number of Alg.2 queries and CEM sample-passes. Used by
  * bench.py to report ALU roofline numbers. Returns GPOEO_OK. */

@@ -24,7 +24,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gpoeo_oracle.c")
 _SO = os.path.join(_HERE, "liboracle.so")
 
-TRACE_OK, TRACE_APERIODIC, TRACE_INSUFFICIENT, TRACE_CONSTANT = 0, 1, 2, 3
+TRACE_OK, TRACE_APERIODIC, TRACE_INSUFFICIENT, TRACE_CONSTANT, TRACE_UNSTABLE = 0, 1, 2, 3, 4
 
 
 class OrParams(ctypes.Structure):
@@ -87,6 +87,12 @@ class OrRolling(ctypes.Structure):
                 ("sub_period", ctypes.c_int32 * 64), ("sub_err", ctypes.c_double * 64)]
 
 
+class OrMeasure(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("t_iter", ctypes.c_int32), ("rounds", ctypes.c_int32),
+                ("samples", ctypes.c_int32), ("measure_start", ctypes.c_int32), ("measure_end", ctypes.c_int32),
+                ("err_iter", ctypes.c_double)]
+
+
 def build() -> str:
     """Compile the oracle (gcc, fp64, no FMA contraction). Building the checker is not using it."""
     if not (os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC)):
@@ -130,6 +136,10 @@ def _L():
                                        ctypes.c_double, ctypes.c_double, ctypes.POINTER(OrRolling)]
         lib.oracle_rolling.restype = ctypes.c_int
         assert lib.oracle_sizeof_rolling() == ctypes.sizeof(OrRolling)
+        lib.oracle_measure.argtypes = [P, ctypes.POINTER(OrParams), P, ctypes.c_int32, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.POINTER(OrMeasure)]
+        lib.oracle_measure.restype = ctypes.c_int
+        assert lib.oracle_sizeof_measure() == ctypes.sizeof(OrMeasure)
         assert lib.oracle_sizeof_params() == ctypes.sizeof(OrParams)
         assert lib.oracle_sizeof_result() == ctypes.sizeof(OrResult)
         _lib = lib
@@ -375,3 +385,17 @@ def rolling(x: np.ndarray, params: Params, c_measure: float = 2.0, step: float =
     return Rolling(status=r.status, t_init=r.t_init, t_iter=r.t_iter, early=bool(r.early), diff=r.diff,
                    smpdur_next=r.smpdur_next, sub_start=list(r.sub_start[:n]), sub_period=list(r.sub_period[:n]),
                    sub_err=list(r.sub_err[:n]))
+
+
+def measure(x: np.ndarray, params: Params, init: int, c_measure: float = 2.0, step: float = 0.5,
+            c_eval: float = 6.5, diff_threshold: float = 0.05) -> dict:
+    """M1: Alg. 4 on one recorded trace x float32 [F][N_max] (reading R6)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    p = params.c()
+    m = OrMeasure()
+    w = None if params.weights is None else np.asarray(params.weights, np.float32).astype(np.float64)
+    if _L().oracle_measure(_ptr(x), ctypes.byref(p), None if w is None else _ptr(w), init, c_measure, step, c_eval,
+                           diff_threshold, ctypes.byref(m)) != 0:
+        raise ValueError("oracle_measure: invalid parameters")
+    return dict(status=m.status, t_iter=m.t_iter, rounds=m.rounds, samples=m.samples,
+                measure_start=m.measure_start, measure_end=m.measure_end, err_iter=m.err_iter)

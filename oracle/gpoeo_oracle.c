@@ -27,6 +27,7 @@
  *   O9 exhaustive search (tests only)
  *   S1 spectral-only detector (T_iter = 1/f_major)
  *   R1 Alg. 3 rolling detector on a recorded trace
+ *   M1 Alg. 4 adaptive measurement on a simulated sampling backend (8f row 3)
  *
  * Pins (tests/test_oracle_*.py): O1 closed-form z-scores; O2 numpy.fft.rfft,
  * Parseval, pure tones, impulse; O3 hand spectra and scipy find_peaks;
@@ -710,6 +711,73 @@ int oracle_rolling(const float* x, const or_params* p, const double* weights, do
   return 0;
 }
 int oracle_sizeof_rolling(void) { return (int)sizeof(or_rolling); }
+
+/* ------------------------------------------------------------------------ */
+/* M1. Alg. 4 lines 1-9, adaptive feature measurement, with a
+ * recorded trace x[F][N_max] as the simulated sampling backend. Reading R6:
+ * the session starts with n = init samples (SmpDur_init); each round runs Alg. 3 (R1) on the
+ * first n samples (Alg. 1's L_max clipped to n/2, Z21) and, while SmpDur_next > 0 (samples),
+ * waits: n += SmpDur_next; SmpDur_next <= 0 ends the loop (T_iter). A session whose next n
+ * would exceed N_max ends UNSTABLE (status 4) with its last T_iter. Lines 8-9: the feature
+ * measurement restarts at sample n and stops after T_iter samples. */
+#define OR_TRACE_UNSTABLE 4
+typedef struct {
+  int32_t status;
+  int32_t t_iter;
+  int32_t rounds;
+  int32_t samples;
+  int32_t measure_start;
+  int32_t measure_end;
+  double err_iter;
+} or_measure;
+
+int oracle_measure(const float* x, const or_params* p, const double* weights, int32_t init, double c_measure,
+                   double step, double c_eval, double diff_threshold, or_measure* out) {
+  memset(out, 0, sizeof(*out));
+  const int32_t Nmax = p->n_samples, F = p->n_features;
+  if (init < 8 || init > Nmax) return -1;
+  out->t_iter = -1;
+  out->measure_start = out->measure_end = -1;
+  float* pre = (float*)malloc(sizeof(float) * (size_t)F * Nmax);
+  int32_t n = init;
+  for (;;) {
+    for (int c = 0; c < F; ++c) memcpy(pre + (size_t)c * n, x + (size_t)c * Nmax, sizeof(float) * n);
+    or_params q = *p;
+    q.n_samples = n;
+    if (q.max_period > n / 2) q.max_period = n / 2;
+    or_rolling r;
+    out->rounds++;
+    out->samples = n;
+    if (q.min_period > q.max_period) {
+      out->status = OR_TRACE_INSUFFICIENT;
+      out->t_iter = -1;
+      break;
+    }
+    if (oracle_rolling(pre, &q, weights, c_measure, step, c_eval, diff_threshold, &r) != 0) {
+      free(pre);
+      return -1;
+    }
+    out->status = r.status;
+    out->t_iter = r.t_iter;
+    out->err_iter = r.err_iter;
+    if (r.status == OR_TRACE_OK && r.smpdur_next > 0.0) {
+      if ((double)n + r.smpdur_next > (double)Nmax) {
+        out->status = OR_TRACE_UNSTABLE;
+        break;
+      }
+      n += (int32_t)r.smpdur_next;
+      continue;
+    }
+    break;
+  }
+  if (out->t_iter > 0) {
+    out->measure_start = n;
+    out->measure_end = n + out->t_iter;
+  }
+  free(pre);
+  return 0;
+}
+int oracle_sizeof_measure(void) { return (int)sizeof(or_measure); }
 
 /* O9 (tests only): Err(L) for every L in [L_min, L_max] of an already-formed
  * signal y; returns the global argmin (Err, L). */

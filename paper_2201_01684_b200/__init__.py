@@ -50,9 +50,12 @@ DETAIL_DTYPE = np.dtype([("n_candidates", "<i4"), ("best_bin", "<i4"), ("local_l
                          ("best_err", "<f8")])
 ROLLING_DTYPE = np.dtype([("status", "<i4"), ("t_init", "<i4"), ("t_iter", "<i4"), ("n_sub", "<i4"),
                           ("early", "<i4"), ("diff", "<f4"), ("smpdur_next_s", "<f4"), ("err_iter", "<f4")])
+MEASURE_DTYPE = np.dtype([("status", "<i4"), ("t_iter", "<i4"), ("rounds", "<i4"), ("samples", "<i4"),
+                          ("measure_start", "<i4"), ("measure_end", "<i4"), ("t_iter_s", "<f4"), ("err_iter", "<f4")])
+TRACE_UNSTABLE = 4
 MAJOR_DTYPE = np.dtype([("period", "<i4"), ("period_s", "<f4"), ("bin", "<i4"), ("status", "<i4")])
 assert RESULT_DTYPE.itemsize == 24 and DETAIL_DTYPE.itemsize == 664 and MAJOR_DTYPE.itemsize == 16
-assert ROLLING_DTYPE.itemsize == 32
+assert ROLLING_DTYPE.itemsize == 32 and MEASURE_DTYPE.itemsize == 32
 
 
 class GpoeoRollingParams(ctypes.Structure):
@@ -118,6 +121,10 @@ def load():
     lib.gpoeo_workspace_size_rolling.restype = ctypes.c_size_t
     lib.gpoeo_detect_rolling.argtypes = [P, ctypes.c_int64, PP, RP, P, P, ctypes.c_size_t, P]
     lib.gpoeo_detect_rolling.restype = ctypes.c_int
+    lib.gpoeo_workspace_size_measure.argtypes = [PP, RP, ctypes.c_int64]
+    lib.gpoeo_workspace_size_measure.restype = ctypes.c_size_t
+    lib.gpoeo_measure_adaptive.argtypes = [P, ctypes.c_int64, PP, RP, ctypes.c_int32, P, P, ctypes.c_size_t, P]
+    lib.gpoeo_measure_adaptive.restype = ctypes.c_int
     lib.gpoeo_read_counters.argtypes = [P, PP, ctypes.c_int64, ctypes.POINTER(GpoeoCounters), P]
     lib.gpoeo_read_counters.restype = ctypes.c_int
     lib.gpoeo_status_string.argtypes = [ctypes.c_int]
@@ -338,6 +345,28 @@ def detect_rolling(traces, p: GpoeoParams, rp: GpoeoRollingParams | None = None,
                                   _stream_handle(stream))
     _check(rc, "gpoeo_detect_rolling")
     return out.cpu().numpy().view(ROLLING_DTYPE)
+
+
+def measure_adaptive(traces, p: GpoeoParams, init_samples: int, rp: GpoeoRollingParams | None = None,
+                     stream=None) -> np.ndarray:
+    """Alg. 4 (reading R6) over recordings [B][trace_stride] on the device (the
+    simulated sampling backend); synchronous; returns MEASURE_DTYPE records."""
+    import torch
+    assert traces.is_cuda and traces.dtype == torch.float32 and traces.is_contiguous()
+    B = traces.shape[0]
+    lib = load()
+    rp = rp or default_rolling_params()
+    need = int(lib.gpoeo_workspace_size_measure(ctypes.byref(p), ctypes.byref(rp), B))
+    if need == 0:
+        _check(validate(p), "params")
+        raise GpoeoError("invalid rolling parameters")
+    ws = alloc_workspace(need, traces.device)
+    out = np.empty(B, dtype=MEASURE_DTYPE)
+    rc = lib.gpoeo_measure_adaptive(ctypes.c_void_p(traces.data_ptr()), B, ctypes.byref(p), ctypes.byref(rp),
+                                    int(init_samples), ctypes.c_void_p(out.ctypes.data),
+                                    ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_handle(stream))
+    _check(rc, "gpoeo_measure_adaptive")
+    return out
 
 
 def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:

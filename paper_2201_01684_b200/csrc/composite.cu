@@ -34,11 +34,12 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
   __shared__ double red[kCompThreads / 32];
   const int64_t t = blockIdx.x;
   if (plan.row_n) N = plan.row_n[t];  // ragged batch: this row's length
-  const float* xt = x + t * stride;
+  const float* xt = x + (plan.row_idx ? (int64_t)plan.row_idx[t] : t) * stride;
+  const int64_t cs = plan.cstride;     // channel c of the trace at xt + c * cs
   float m[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
   bool all_const = true;
   for (int c = 0; c < F; ++c) {
-    const float* xc = xt + (int64_t)c * N;
+    const float* xc = xt + (int64_t)c * cs;
     const double x0 = (double)__ldg(xc);
     double s = 0.0, q = 0.0;
     if ((N & 3) == 0) {
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
       float v[4] = {0.f, 0.f, 0.f, 0.f};
       for (int c = 0; c < F; ++c) {
         if (a[c] == 0.f) continue;
-        float4 xv = __ldg(reinterpret_cast<const float4*>(xt + (int64_t)c * N) + i);
+        float4 xv = __ldg(reinterpret_cast<const float4*>(xt + (int64_t)c * cs) + i);
         v[0] = __fadd_rn(v[0], __fmul_rn(a[c], __fsub_rn(xv.x, m[c])));
         v[1] = __fadd_rn(v[1], __fmul_rn(a[c], __fsub_rn(xv.y, m[c])));
         v[2] = __fadd_rn(v[2], __fmul_rn(a[c], __fsub_rn(xv.z, m[c])));
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
     for (int i = threadIdx.x; i < N; i += kCompThreads) {
       float v = 0.f;
       for (int c = 0; c < F; ++c)
-        if (a[c] != 0.f) v = __fadd_rn(v, __fmul_rn(a[c], __fsub_rn(__ldg(xt + (int64_t)c * N + i), m[c])));
+        if (a[c] != 0.f) v = __fadd_rn(v, __fmul_rn(a[c], __fsub_rn(__ldg(xt + (int64_t)c * cs + i), m[c])));
       yt[i] = v;
     }
   }

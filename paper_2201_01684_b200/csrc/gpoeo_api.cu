@@ -82,6 +82,8 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
   pl.batch = batch;
   pl.ystride = pl.N;
   pl.row_n = nullptr;
+  pl.cstride = pl.N;
+  pl.row_idx = nullptr;
   // band (Z21): floor(N/k) <= Lmax  <=>  k >= floor(N/(Lmax+1)) + 1;  floor(N/k) >= Lmin <=> k <= floor(N/Lmin)
   int64_t klo = (int64_t)pl.N / ((int64_t)pl.Lmax + 1) + 1;
   int64_t khi = (int64_t)pl.N / pl.Lmin;
@@ -255,7 +257,16 @@ struct RollLayout {
   int64_t max_sub;
 };
 
-static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t B) {
+// ragged: the whole traces have per-trace lengths <= N (Alg. 4 prefixes): their local
+// ranges are bounded by the band instead of by N's
+static Plan main_plan(const gpoeo_params* p, int64_t B, bool ragged) {
+  Plan pm = make_plan(p, B);
+  if (ragged) pm.max_local = (int64_t)pm.Lmax - pm.Lmin + 1;
+  return pm;
+}
+
+static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t B,
+                                 bool ragged = false) {
   RollLayout R;
   R.max_sub = rolling_max_sub(rp);
   size_t o = 0;
@@ -264,7 +275,7 @@ static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_para
     o = align_up(o + bytes);
     return r;
   };
-  R.main = take(layout(make_plan(p, B)).total);
+  R.main = take(layout(main_plan(p, B, ragged)).total);
   R.whole = take(sizeof(gpoeo_result) * (size_t)B);
   R.plan = take(sizeof(RollTrace) * (size_t)B);
   R.segs = take(sizeof(RollSeg) * (size_t)B * (size_t)R.max_sub);
@@ -282,6 +293,117 @@ static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_para
   R.gws = take(layout(pl).total);
   R.total = o;
   return R;
+}
+
+// Alg. 3 on `batch` traces (whole traces, or with host_len: row t = the first host_len[t]
+// samples of trace dev_idx[t], dev_len a device copy of host_len); R laid out for it.
+static int rolling_core(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
+                        const int32_t* host_len, const int32_t* dev_len, const int32_t* dev_idx,
+                        gpoeo_rolling_result* results, char* b, const RollLayout& R, cudaStream_t s) {
+  // line 1: T_init = Alg. 1 on every whole trace (the composite y stays in the workspace)
+  Plan pm = main_plan(p, batch, host_len != nullptr);
+  if (host_len) {  // ragged whole traces: row t = trace idx[t], its first len[t] samples of every channel
+    pm.row_n = dev_len;
+    pm.row_idx = dev_idx;
+  }
+  const Layout Lm = layout(pm);
+  gpoeo_result* whole = reinterpret_cast<gpoeo_result*>(b + R.whole);
+  int rc = run_detect(traces, pm, Lm, b + R.main, whole, nullptr, s);
+  if (rc != GPOEO_OK) return rc;
+  const float* y = carve(pm, Lm, b + R.main).y;
+  std::vector<gpoeo_result> hw((size_t)batch);
+  CK(cudaMemcpyAsync(hw.data(), whole, sizeof(gpoeo_result) * (size_t)batch, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // lines 2-13 on the host (exact sample arithmetic, as the oracle): the suffix plan
+  const int32_t N = p->n_samples;  // row stride of y
+  std::vector<RollTrace> plan((size_t)batch);
+  std::vector<int32_t> sfx_trace, sfx_start;
+  for (int64_t t = 0; t < batch; ++t) {
+    RollTrace& pt = plan[(size_t)t];
+    pt.first = (int32_t)sfx_trace.size();
+    pt.n_sub = 0;
+    pt.early = 0;
+    pt.pad = 0;
+    if (hw[(size_t)t].status != GPOEO_TRACE_OK) continue;
+    const int32_t Nt = host_len ? host_len[t] : N;
+    const double smpdur = (double)(Nt - 1);
+    const double L0 = (double)hw[(size_t)t].period;
+    if (smpdur < rp->c_measure * L0) {
+      pt.early = 1;
+      continue;
+    }
+    double ts = smpdur - (2.0 + rp->c_eval * rp->step) * L0;
+    if (ts < 0.0) ts = 0.0;
+    while ((smpdur - ts) / L0 >= rp->c_measure && pt.n_sub < R.max_sub) {
+      const int32_t s0 = (int32_t)floor(ts);
+      sfx_trace.push_back((int32_t)t);
+      sfx_start.push_back(s0);
+      ++pt.n_sub;
+      ts += rp->step * L0;
+    }
+  }
+  RollTrace* dplan = reinterpret_cast<RollTrace*>(b + R.plan);
+  RollSeg* dsegs = reinterpret_cast<RollSeg*>(b + R.segs);
+  CK(cudaMemcpyAsync(dplan, plan.data(), sizeof(RollTrace) * (size_t)batch, cudaMemcpyHostToDevice, s));
+  if (!sfx_trace.empty())
+    CK(cudaMemsetAsync(dsegs, 0xFF, sizeof(RollSeg) * sfx_trace.size(), s));  // period -1: none
+  // Alg. 1 on every suffix (line 11): the suffixes, each a one-channel sequence of its own
+  // length, run as ragged batches of up to `batch` rows (per-row N: Plan::row_n)
+  int32_t* gtrace = reinterpret_cast<int32_t*>(b + R.gtrace);
+  int32_t* gstart = reinterpret_cast<int32_t*>(b + R.gstart);
+  int32_t* gseg = reinterpret_cast<int32_t*>(b + R.gseg);
+  int32_t* grown = reinterpret_cast<int32_t*>(b + R.grown);
+  float* gsig = reinterpret_cast<float*>(b + R.gsig);
+  gpoeo_result* gres = reinterpret_cast<gpoeo_result*>(b + R.gres);
+  gpoeo_detail* gdet = reinterpret_cast<gpoeo_detail*>(b + R.gdet);
+  // suffixes shorter than the smallest supported sequence (8 samples) find no period (the
+  // oracle rejects them too)
+  std::vector<int32_t> run_trace, run_start, run_seg, run_len;
+  for (size_t i = 0; i < sfx_trace.size(); ++i) {
+    const int32_t Nt = host_len ? host_len[sfx_trace[i]] : N;
+    if (Nt - sfx_start[i] >= (1 << GPOEO_MIN_LOG2N)) {
+      run_trace.push_back(sfx_trace[i]);
+      run_start.push_back(sfx_start[i]);
+      run_seg.push_back((int32_t)i);
+      run_len.push_back(Nt - sfx_start[i]);
+    }
+  }
+  const int64_t nrun = (int64_t)run_seg.size();
+  std::vector<int32_t> hn;
+  for (int64_t c0 = 0; c0 < nrun; c0 += batch) {
+    const int32_t n = (int32_t)(nrun - c0 < batch ? nrun - c0 : batch);
+    hn.resize(n);
+    int32_t Smax = 0;
+    for (int32_t r = 0; r < n; ++r) {
+      hn[r] = run_len[c0 + r];
+      if (hn[r] > Smax) Smax = hn[r];
+    }
+    const int32_t S = (Smax + 3) & ~3;
+    const gpoeo_params q = suffix_params(p, S);
+    if (q.min_period > q.max_period) continue;  // every row too short for L_min: no period (as the oracle)
+    CK(cudaMemcpyAsync(gtrace, run_trace.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(gstart, run_start.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(grown, hn.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(gseg, run_seg.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    CK(launch_gather_suffix_ragged(y, N, gtrace, gstart, grown, n, S, gsig, s));
+    Plan pr = make_plan(&q, n);
+    pr.row_n = grown;
+    pr.max_local = (int64_t)q.max_period - q.min_period + 1;  // rows clip L_max to N_j/2: bound
+    const Layout Lr = layout(pr);
+    if (Lr.total > R.total - R.gws) return GPOEO_ERR_WORKSPACE;  // not expected: R.gws bounds it
+    if (band_smem_bytes(pr, false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
+    rc = run_detect(gsig, pr, Lr, b + R.gws, gres, gdet, s);
+    if (rc != GPOEO_OK) return rc;
+    CK(launch_scatter_suffix(gres, gdet, n, gseg, dsegs, s));
+    // the host vectors are rewritten by the next chunk: pageable H2D copies are staged before
+    // cudaMemcpyAsync returns
+  }
+  // lines 14-21
+  RollParamsDev rpd{rp->c_measure, rp->step, rp->c_eval, rp->diff_threshold};
+  CK(launch_rolling_final(batch, N, host_len ? dev_len : nullptr, p->sample_interval, rpd, whole, dplan, dsegs,
+                          results, s));
+  CK(cudaStreamSynchronize(s));
+  return GPOEO_OK;
 }
 
 }  // namespace
@@ -541,101 +663,112 @@ int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params*
   if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
   if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
   if (batch == 0) return GPOEO_OK;
+  return rolling_core(traces, batch, p, rp, nullptr, nullptr, nullptr, results, static_cast<char*>(workspace), R,
+                      static_cast<cudaStream_t>(stream));
+}
+
+// ---- Alg. 4 adaptive measurement (reading R6) -------------------------
+struct MeasureLayout {
+  RollLayout R;
+  size_t len, idx, res, total;
+};
+
+static MeasureLayout measure_layout(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t B) {
+  MeasureLayout M;
+  M.R = rolling_layout(p, rp, B, true);
+  size_t o = M.R.total;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  M.len = take(sizeof(int32_t) * (size_t)B);
+  M.idx = take(sizeof(int32_t) * (size_t)B);
+  M.res = take(sizeof(gpoeo_rolling_result) * (size_t)B);
+  M.total = o;
+  return M;
+}
+
+size_t gpoeo_workspace_size_measure(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t batch) {
+  if (validate(p) != GPOEO_OK || validate_rolling(rp) != GPOEO_OK || batch < 0) return 0;
+  return measure_layout(p, rp, batch).total;
+}
+
+int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
+                           int32_t init_samples, gpoeo_measure_result* results, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  v = validate_rolling(rp);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0 || batch >= (1ll << 31)) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (batch > 0 && (!traces || !results)) return GPOEO_ERR_INVALID_ARGUMENT;
+  const int32_t Nmax = p->n_samples;
+  if (init_samples < (1 << GPOEO_MIN_LOG2N) || init_samples > Nmax) return GPOEO_ERR_INVALID_ARGUMENT;
+  const MeasureLayout M = measure_layout(p, rp, batch);
+  if (!workspace || workspace_bytes < M.total) return GPOEO_ERR_WORKSPACE;
+  if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  if (batch == 0) return GPOEO_OK;
+  if (band_smem_bytes(main_plan(p, batch, true), false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* b = static_cast<char*>(workspace);
-  // line 1: T_init = Alg. 1 on every whole trace (the composite y stays in the workspace)
-  const Plan pm = make_plan(p, batch);
-  const Layout Lm = layout(pm);
-  gpoeo_result* whole = reinterpret_cast<gpoeo_result*>(b + R.whole);
-  int rc = run_detect(traces, pm, Lm, b + R.main, whole, nullptr, s);
-  if (rc != GPOEO_OK) return rc;
-  const float* y = carve(pm, Lm, b + R.main).y;
-  std::vector<gpoeo_result> hw((size_t)batch);
-  CK(cudaMemcpyAsync(hw.data(), whole, sizeof(gpoeo_result) * (size_t)batch, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  // lines 2-13 on the host (exact sample arithmetic, as the oracle): the suffix plan
-  const int32_t N = p->n_samples;
-  const double smpdur = (double)(N - 1);
-  std::vector<RollTrace> plan((size_t)batch);
-  std::vector<int32_t> sfx_trace, sfx_start;
+  int32_t* dlen = reinterpret_cast<int32_t*>(b + M.len);
+  int32_t* didx = reinterpret_cast<int32_t*>(b + M.idx);
+  gpoeo_rolling_result* dres = reinterpret_cast<gpoeo_rolling_result*>(b + M.res);
+  std::vector<int32_t> n((size_t)batch, init_samples), act, alen;
+  std::vector<gpoeo_rolling_result> hr;
   for (int64_t t = 0; t < batch; ++t) {
-    RollTrace& pt = plan[(size_t)t];
-    pt.first = (int32_t)sfx_trace.size();
-    pt.n_sub = 0;
-    pt.early = 0;
-    pt.pad = 0;
-    if (hw[(size_t)t].status != GPOEO_TRACE_OK) continue;
-    const double L0 = (double)hw[(size_t)t].period;
-    if (smpdur < rp->c_measure * L0) {
-      pt.early = 1;
-      continue;
-    }
-    double ts = smpdur - (2.0 + rp->c_eval * rp->step) * L0;
-    if (ts < 0.0) ts = 0.0;
-    while ((smpdur - ts) / L0 >= rp->c_measure && pt.n_sub < R.max_sub) {
-      const int32_t s0 = (int32_t)floor(ts);
-      sfx_trace.push_back((int32_t)t);
-      sfx_start.push_back(s0);
-      ++pt.n_sub;
-      ts += rp->step * L0;
-    }
+    gpoeo_measure_result& r = results[t];
+    r.status = GPOEO_TRACE_OK;
+    r.t_iter = -1;
+    r.rounds = 0;
+    r.samples = init_samples;
+    r.measure_start = r.measure_end = -1;
+    r.t_iter_s = -1.f;
+    r.err_iter = 0.f;
+    act.push_back((int32_t)t);
   }
-  RollTrace* dplan = reinterpret_cast<RollTrace*>(b + R.plan);
-  RollSeg* dsegs = reinterpret_cast<RollSeg*>(b + R.segs);
-  CK(cudaMemcpyAsync(dplan, plan.data(), sizeof(RollTrace) * (size_t)batch, cudaMemcpyHostToDevice, s));
-  if (!sfx_trace.empty())
-    CK(cudaMemsetAsync(dsegs, 0xFF, sizeof(RollSeg) * sfx_trace.size(), s));  // period -1: none
-  // Alg. 1 on every suffix (line 11): the suffixes, each a one-channel sequence of its own
-  // length, run as ragged batches of up to `batch` rows (per-row N: Plan::row_n)
-  int32_t* gtrace = reinterpret_cast<int32_t*>(b + R.gtrace);
-  int32_t* gstart = reinterpret_cast<int32_t*>(b + R.gstart);
-  int32_t* gseg = reinterpret_cast<int32_t*>(b + R.gseg);
-  int32_t* grown = reinterpret_cast<int32_t*>(b + R.grown);
-  float* gsig = reinterpret_cast<float*>(b + R.gsig);
-  gpoeo_result* gres = reinterpret_cast<gpoeo_result*>(b + R.gres);
-  gpoeo_detail* gdet = reinterpret_cast<gpoeo_detail*>(b + R.gdet);
-  // suffixes shorter than the smallest supported sequence (8 samples) find no period (the
-  // oracle rejects them too)
-  std::vector<int32_t> run_trace, run_start, run_seg;
-  for (size_t i = 0; i < sfx_trace.size(); ++i)
-    if (N - sfx_start[i] >= (1 << GPOEO_MIN_LOG2N)) {
-      run_trace.push_back(sfx_trace[i]);
-      run_start.push_back(sfx_start[i]);
-      run_seg.push_back((int32_t)i);
-    }
-  const int64_t nrun = (int64_t)run_seg.size();
-  std::vector<int32_t> hn;
-  for (int64_t c0 = 0; c0 < nrun; c0 += batch) {
-    const int32_t n = (int32_t)(nrun - c0 < batch ? nrun - c0 : batch);
-    hn.resize(n);
-    int32_t Smax = 0;
-    for (int32_t r = 0; r < n; ++r) {
-      hn[r] = N - run_start[c0 + r];
-      if (hn[r] > Smax) Smax = hn[r];
-    }
-    const int32_t S = (Smax + 3) & ~3;
-    const gpoeo_params q = suffix_params(p, S);
-    if (q.min_period > q.max_period) continue;  // every row too short for L_min: no period (as the oracle)
-    CK(cudaMemcpyAsync(gtrace, run_trace.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(gstart, run_start.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(grown, hn.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(gseg, run_seg.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(launch_gather_suffix_ragged(y, N, gtrace, gstart, grown, n, S, gsig, s));
-    Plan pr = make_plan(&q, n);
-    pr.row_n = grown;
-    pr.max_local = (int64_t)q.max_period - q.min_period + 1;  // rows clip L_max to N_j/2: bound
-    const Layout Lr = layout(pr);
-    if (Lr.total > R.total - R.gws) return GPOEO_ERR_WORKSPACE;  // not expected: R.gws bounds it
-    if (band_smem_bytes(pr, false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
-    rc = run_detect(gsig, pr, Lr, b + R.gws, gres, gdet, s);
+  while (!act.empty()) {
+    // one round: Alg. 3 on every unfinished session's samples so far (one ragged batch)
+    const int32_t na = (int32_t)act.size();
+    alen.resize(na);
+    for (int32_t i = 0; i < na; ++i) alen[i] = n[act[i]];
+    CK(cudaMemcpyAsync(dlen, alen.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(didx, act.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
+    int rc = rolling_core(traces, na, p, rp, alen.data(), dlen, didx, dres, b, M.R, s);
     if (rc != GPOEO_OK) return rc;
-    CK(launch_scatter_suffix(gres, gdet, n, gseg, dsegs, s));
-    // the host vectors are rewritten by the next chunk: pageable H2D copies are staged before
-    // cudaMemcpyAsync returns
+    hr.resize(na);
+    CK(cudaMemcpy(hr.data(), dres, sizeof(gpoeo_rolling_result) * na, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> next;
+    for (int32_t i = 0; i < na; ++i) {
+      const int32_t t = act[i];
+      gpoeo_measure_result& r = results[t];
+      const gpoeo_rolling_result& q = hr[i];
+      r.rounds += 1;
+      r.status = q.status;
+      r.t_iter = q.t_iter;
+      r.err_iter = q.err_iter;
+      r.samples = n[t];
+      // SmpDur_next back in samples (an integer: lines 5, 21 and R5's fallback)
+      const double more = q.smpdur_next_s < 0.f ? -1.0 : rint((double)q.smpdur_next_s / p->sample_interval);
+      if (more > 0.0 && q.status == GPOEO_TRACE_OK) {
+        if ((double)n[t] + more > (double)Nmax) {
+          r.status = GPOEO_TRACE_UNSTABLE;  // the recording ends before T_iter is stable
+        } else {
+          n[t] += (int32_t)more;
+          next.push_back(t);
+          continue;
+        }
+      }
+      if (r.t_iter > 0) {  // lines 8-9: restart the measurement now, stop after T_iter
+        r.measure_start = n[t];
+        r.measure_end = n[t] + r.t_iter;
+        r.t_iter_s = (float)((double)r.t_iter * p->sample_interval);
+      }
+    }
+    act.swap(next);
   }
-  // lines 14-21
-  RollParamsDev rpd{rp->c_measure, rp->step, rp->c_eval, rp->diff_threshold};
-  CK(launch_rolling_final(batch, N, p->sample_interval, rpd, whole, dplan, dsegs, results, s));
   CK(cudaStreamSynchronize(s));
   return GPOEO_OK;
 }

@@ -29,7 +29,9 @@ struct Plan {
   int64_t max_local;          // per-trace upper bound on the local-range size
   int64_t batch;
   int64_t ystride;            // floats between rows of the composite signal y (N when uniform)
-  const int32_t* row_n;       // ragged batch (Alg. 3 suffixes, F = 1): per-row N, or null
+  const int32_t* row_n;       // ragged batch (Alg. 3 suffixes, Alg. 4 prefixes): per-row N, or null
+  int64_t cstride;            // floats between the feature channels of a trace (N when uniform)
+  const int32_t* row_idx;     // row t reads trace row_idx[t] of the input (null: t)
 };
 
 // The plan of row t: a ragged batch carries its own N per row (L_max clipped to N/2, the
@@ -182,9 +184,9 @@ cudaError_t launch_gather_suffix_ragged(const float* y, int32_t N, const int32_t
                                         const int32_t* len, int32_t n, int64_t stride, float* dst, cudaStream_t s);
 cudaError_t launch_scatter_suffix(const gpoeo_result* res, const gpoeo_detail* det, int32_t n, const int32_t* seg,
                                   RollSeg* out, cudaStream_t s);
-cudaError_t launch_rolling_final(int64_t batch, int32_t N, double Ts, RollParamsDev rp, const gpoeo_result* whole,
-                                 const RollTrace* plan, const RollSeg* segs, gpoeo_rolling_result* out,
-                                 cudaStream_t s);
+cudaError_t launch_rolling_final(int64_t batch, int32_t N, const int32_t* row_n, double Ts, RollParamsDev rp,
+                                 const gpoeo_result* whole, const RollTrace* plan, const RollSeg* segs,
+                                 gpoeo_rolling_result* out, cudaStream_t s);
 cudaError_t launch_final(const Plan& p, Work w, gpoeo_result* results, gpoeo_detail* detail, cudaStream_t s);
 
 

@@ -33,11 +33,13 @@ __global__ void scatter_suffix_kernel(const gpoeo_result* __restrict__ res, cons
 
 // Alg. 3 lines 14-21 per trace (one thread per trace): T_iter = T_k of the smallest err
 // (ties: smaller T, Z17), Diff = |max T - min T| / mean T, SmpDur_next (samples -> seconds)
-__global__ void rolling_final_kernel(int64_t batch, int32_t N, double Ts, RollParamsDev rp,
+__global__ void rolling_final_kernel(int64_t batch, int32_t Nu, const int32_t* __restrict__ row_n, double Ts,
+                                     RollParamsDev rp,
                                      const gpoeo_result* __restrict__ whole, const RollTrace* __restrict__ plan,
                                      const RollSeg* __restrict__ segs, gpoeo_rolling_result* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= batch) return;
+  const int32_t N = row_n ? row_n[t] : Nu;
   gpoeo_rolling_result r;
   const gpoeo_result w = whole[t];
   const RollTrace pt = plan[t];
@@ -104,11 +106,12 @@ cudaError_t launch_scatter_suffix(const gpoeo_result* res, const gpoeo_detail* d
   return cudaGetLastError();
 }
 
-cudaError_t launch_rolling_final(int64_t batch, int32_t N, double Ts, RollParamsDev rp, const gpoeo_result* whole,
-                                 const RollTrace* plan, const RollSeg* segs, gpoeo_rolling_result* out,
-                                 cudaStream_t s) {
+cudaError_t launch_rolling_final(int64_t batch, int32_t N, const int32_t* row_n, double Ts, RollParamsDev rp,
+                                 const gpoeo_result* whole, const RollTrace* plan, const RollSeg* segs,
+                                 gpoeo_rolling_result* out, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  rolling_final_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(batch, N, Ts, rp, whole, plan, segs, out);
+  rolling_final_kernel<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(batch, N, row_n, Ts, rp, whole, plan, segs,
+                                                                      out);
   return cudaGetLastError();
 }
 

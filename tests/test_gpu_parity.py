@@ -517,3 +517,41 @@ def test_rolling_period_shift():
     # mid-trace period change (config 5's structure at N = 8192): the suffixes see the new period
     spec = tg.CFG5.with_(batch=6, n_samples=8192, period_lo=30.0, period_hi=200.0, max_period=2048)
     _rolling_compare(tg.generate_host(spec), spec, "shift")
+
+
+# ---- Alg. 4 adaptive measurement (oracle M1, reading R6) ----------------
+
+def _measure_compare(x, spec, init, label):
+    r = g.measure_adaptive(_to_dev(x), g.params_for(spec), init)
+    op = O.params_for(spec, dft_band_only=True)
+    bad = []
+    for i in range(x.shape[0]):
+        o = O.measure(x[i], op, init)
+        got = (int(r[i]["status"]), int(r[i]["t_iter"]), int(r[i]["rounds"]), int(r[i]["samples"]),
+               int(r[i]["measure_start"]), int(r[i]["measure_end"]))
+        want = (o["status"], o["t_iter"], o["rounds"], o["samples"], o["measure_start"], o["measure_end"])
+        if got != want:
+            bad.append((i, got, want))
+    # a near-tie inside any round's Alg. 1 (Z27) may legitimately change the trajectory
+    assert len(bad) <= max(1, x.shape[0] // 8), (label, bad)
+    return r
+
+
+def test_measure_config1_and_closed_form():
+    r = _measure_compare(tg.generate_host(tg.CFG1), tg.CFG1, 1024, "cfg1")
+    assert (r[0]["t_iter"], r[0]["rounds"], r[0]["samples"]) == (37, 1, 1024)
+    n = np.arange(2048)
+    x = (np.where((n % 20) < 7, 1.0, 0.0) + 0.01 * np.sin(0.37 * n)).astype(np.float32)[None, None]
+    spec = tg.CFG1.with_(n_samples=2048, min_period=4, max_period=1024)
+    r = g.measure_adaptive(_to_dev(x), g.params_for(spec), 40)
+    assert (r[0]["rounds"], r[0]["samples"], r[0]["t_iter"], r[0]["measure_start"]) == (2, 41, 20, 41)
+
+
+def test_measure_config2_slice():
+    spec = tg.CFG2.with_(batch=16)
+    _measure_compare(tg.generate_host(spec), spec, 2048, "cfg2")
+
+
+def test_measure_period_shift():
+    spec = tg.CFG5.with_(batch=6, n_samples=8192, period_lo=30.0, period_hi=200.0, max_period=2048)
+    _measure_compare(tg.generate_host(spec), spec, 2048, "shift")
