@@ -338,6 +338,24 @@ def run_gpu(args) -> None:
             "timing": "wall clock of the synchronous gpoeo_detect_rolling (inputs resident in HBM)",
             "note": "time is dominated by the Alg. 2 scorer kernels of the roofline above (whole traces + suffixes)"}
 
+    # Alg. 4 adaptive measurement: sessions over the same resident recordings,
+    # starting from SmpDur_init = 2 L_max samples; synchronous rounds of ragged Alg. 3 batches
+    if not args.no_rolling:
+        Bm = min(args.rolling_batch, B)
+        init = min(spec.n_samples, 2 * spec.max_period)
+        g.measure_adaptive(x[:Bm], p, init)  # warm
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        mr = g.measure_adaptive(x[:Bm], p, init)
+        tm = _max_over_ranks(time.perf_counter() - t0, dev)
+        line["measure"] = {
+            "metric": "sessions/sec Alg. 4 adaptive measurement (P:431-462)", "value": world * Bm / tm,
+            "unit": "sessions/s", "batch_per_gpu": Bm, "init_samples": init, "ms_per_step": 1e3 * tm,
+            "mean_rounds": float(mr["rounds"].mean()), "mean_samples": float(mr["samples"].mean()),
+            "stable_frac": float((mr["status"] == 0).mean()),
+            "timing": "wall clock of the synchronous gpoeo_measure_adaptive (recordings resident in HBM)"}
+
     # e2e: same metric through the public host entry point (pinned host buffers, H2D+D2H inside)
     del x
     torch.cuda.empty_cache()
