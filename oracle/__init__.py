@@ -93,6 +93,16 @@ class OrMeasure(ctypes.Structure):
                 ("err_iter", ctypes.c_double)]
 
 
+class OrGearWorkload(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("compute_work", "memory_work", "overhead", "p_static", "c_sm",
+                                                 "c_mem", "u_c", "u_m", "noise")] + [("seed", ctypes.c_uint64)]
+
+
+class OrGearResult(ctypes.Structure):
+    _fields_ = [("sm_gear", ctypes.c_int32), ("mem_gear", ctypes.c_int32), ("probes_sm", ctypes.c_int32),
+                ("probes_mem", ctypes.c_int32), ("objective", ctypes.c_double)]
+
+
 def build() -> str:
     """Compile the oracle (gcc, fp64, no FMA contraction). Building the checker is not using it."""
     if not (os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC)):
@@ -140,6 +150,14 @@ def _L():
                                        ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.POINTER(OrMeasure)]
         lib.oracle_measure.restype = ctypes.c_int
         assert lib.oracle_sizeof_measure() == ctypes.sizeof(OrMeasure)
+        lib.oracle_gear_objective.argtypes = [ctypes.POINTER(OrGearWorkload), P, ctypes.c_int32, P, ctypes.c_int32,
+                                              ctypes.c_double, ctypes.c_int32, ctypes.c_int32]
+        lib.oracle_gear_objective.restype = ctypes.c_double
+        lib.oracle_gear_search.argtypes = [ctypes.POINTER(OrGearWorkload), P, ctypes.c_int32, P, ctypes.c_int32,
+                                           ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.POINTER(OrGearResult)]
+        lib.oracle_gear_search.restype = ctypes.c_int
+        assert lib.oracle_sizeof_gear() == ctypes.sizeof(OrGearWorkload) * 1000 + ctypes.sizeof(OrGearResult)
         assert lib.oracle_sizeof_params() == ctypes.sizeof(OrParams)
         assert lib.oracle_sizeof_result() == ctypes.sizeof(OrResult)
         _lib = lib
@@ -399,3 +417,28 @@ def measure(x: np.ndarray, params: Params, init: int, c_measure: float = 2.0, st
         raise ValueError("oracle_measure: invalid parameters")
     return dict(status=m.status, t_iter=m.t_iter, rounds=m.rounds, samples=m.samples,
                 measure_start=m.measure_start, measure_end=m.measure_end, err_iter=m.err_iter)
+
+
+def gear_workload(**kw) -> OrGearWorkload:
+    w = OrGearWorkload()
+    for k, v in kw.items():
+        setattr(w, k, v)
+    return w
+
+
+def gear_objective(w: OrGearWorkload, sm_mhz, mem_mhz, cap: float, gs: int, gm: int) -> float:
+    sm = np.ascontiguousarray(sm_mhz, np.float64)
+    mem = np.ascontiguousarray(mem_mhz, np.float64)
+    return _L().oracle_gear_objective(ctypes.byref(w), _ptr(sm), sm.size, _ptr(mem), mem.size, cap, gs, gm)
+
+
+def gear_search(w: OrGearWorkload, sm_mhz, mem_mhz, cap: float, pred_sm: int, pred_mem: int) -> dict:
+    """G1: memory then SM local search (bracket, golden section, convex fit) on the simulator."""
+    sm = np.ascontiguousarray(sm_mhz, np.float64)
+    mem = np.ascontiguousarray(mem_mhz, np.float64)
+    r = OrGearResult()
+    if _L().oracle_gear_search(ctypes.byref(w), _ptr(sm), sm.size, _ptr(mem), mem.size, cap, pred_sm, pred_mem,
+                               ctypes.byref(r)) != 0:
+        raise ValueError("oracle_gear_search: invalid arguments")
+    return dict(sm_gear=r.sm_gear, mem_gear=r.mem_gear, probes_sm=r.probes_sm, probes_mem=r.probes_mem,
+                objective=r.objective)

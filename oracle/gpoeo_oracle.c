@@ -28,6 +28,7 @@
  *   S1 spectral-only detector (T_iter = 1/f_major)
  *   R1 Alg. 3 rolling detector on a recorded trace
  *   M1 Alg. 4 adaptive measurement on a simulated sampling backend (8f row 3)
+ *   G1 gear local search (bracket, golden section, convex fit; 8f row 4)
  *
  * Pins (tests/test_oracle_*.py): O1 closed-form z-scores; O2 numpy.fft.rfft,
  * Parseval, pure tones, impulse; O3 hand spectra and scipy find_peaks;
@@ -778,6 +779,175 @@ int oracle_measure(const float* x, const or_params* p, const double* weights, in
   return 0;
 }
 int oracle_sizeof_measure(void) { return (int)sizeof(or_measure); }
+
+/* ------------------------------------------------------------------------ */
+/* G1. Online local search of the clock gears against a
+ * simulated device, reading R7 (the paper gives the procedure in prose, the
+ * simulator and the discrete rules follow SPEC's gear-search and gpu-simulator modules):
+ *  - simulator: T(fs, fm) = max(Wc/fs, Wm/fm) + t0, P = Ps + csm u_c fs^1.8 + cmem u_m fm,
+ *    E = P T; relative to the default gears (the highest of each domain): e = E/E0,
+ *    t = T/T0; objective = e + 10 max(0, t - 1 - cap); optional multiplicative noise
+ *    (1 + noise h), h in [-1, 1) from splitmix64(seed ^ (gs << 20) ^ (gm << 4) ^ 0x9E37):
+ *    the same counter-based hash on both sides;
+ *  - memory clock first (at the predicted SM gear), then SM clock at the chosen memory gear;
+ *  - per domain: bracket outward from the predicted gear with doubling strides until a
+ *    strictly worse value (or the boundary) on each side; discrete golden-section search on
+ *    the bracket (probes rounded to the nearest gear, cached, a collision steps one gear
+ *    toward the larger side) until <= 3 gears remain (then probed too, so a bracket ending at
+ *    the boundary probes it) or 12 iterations; then a least-squares quadratic through the
+ *    (up to) 5 probes nearest the best one: a > 0 -> the gear nearest the vertex, clamped to
+ *    those probes' range; otherwise the best probe. */
+typedef struct {
+  double compute_work, memory_work, overhead, p_static, c_sm, c_mem, u_c, u_m, noise;
+  uint64_t seed;
+} or_gear_workload;
+
+typedef struct {
+  int32_t sm_gear, mem_gear, probes_sm, probes_mem;
+  double objective;
+} or_gear_result;
+
+static uint64_t or_splitmix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static void or_sim(const or_gear_workload* w, double fs, double fm, double* T, double* E) {
+  const double a = w->compute_work / fs, b = w->memory_work / fm;
+  *T = (a > b ? a : b) + w->overhead;
+  const double P = w->p_static + w->c_sm * w->u_c * pow(fs, 1.8) + w->c_mem * w->u_m * fm;
+  *E = P * (*T);
+}
+
+double oracle_gear_objective(const or_gear_workload* w, const double* sm_mhz, int32_t n_sm, const double* mem_mhz,
+                             int32_t n_mem, double cap, int32_t gs, int32_t gm) {
+  double T0, E0, T, E;
+  or_sim(w, sm_mhz[n_sm - 1], mem_mhz[n_mem - 1], &T0, &E0);
+  or_sim(w, sm_mhz[gs], mem_mhz[gm], &T, &E);
+  const double t = T / T0, e = E / E0;
+  double o = e + 10.0 * (t - 1.0 - cap > 0.0 ? t - 1.0 - cap : 0.0);
+  if (w->noise != 0.0) {
+    const uint64_t h = or_splitmix(w->seed ^ ((uint64_t)gs << 20) ^ ((uint64_t)gm << 4) ^ 0x9E37ull);
+    const double u = (double)(h >> 11) * (1.0 / 9007199254740992.0); /* [0, 1) */
+    o *= 1.0 + w->noise * (2.0 * u - 1.0);
+  }
+  return o;
+}
+
+typedef struct {
+  const or_gear_workload* w;
+  const double *sm, *mem;
+  int32_t n_sm, n_mem, dom, other; /* dom 0: SM gears vary (mem fixed = other); 1: memory */
+  double cap;
+  double val[256];
+  int32_t probed[256];
+  int32_t count;
+} or_line;
+
+static double or_eval(or_line* L, int32_t g) {
+  if (!L->probed[g]) {
+    L->probed[g] = 1;
+    L->count++;
+    L->val[g] = L->dom == 0 ? oracle_gear_objective(L->w, L->sm, L->n_sm, L->mem, L->n_mem, L->cap, g, L->other)
+                            : oracle_gear_objective(L->w, L->sm, L->n_sm, L->mem, L->n_mem, L->cap, L->other, g);
+  }
+  return L->val[g];
+}
+
+static int32_t or_line_search(or_line* L, int32_t start, int32_t n) {
+  const int32_t max_steps = 12; /* golden-section iterations */
+  const double o0 = or_eval(L, start);
+  int32_t lo = start, hi = start;
+  for (int32_t d = 1;; d *= 2) { /* bracket, low side */
+    const int32_t g = start - d;
+    if (g <= 0) { lo = 0; break; }
+    if (or_eval(L, g) > o0) { lo = g; break; }
+  }
+  for (int32_t d = 1;; d *= 2) { /* high side */
+    const int32_t g = start + d;
+    if (g >= n - 1) { hi = n - 1; break; }
+    if (or_eval(L, g) > o0) { hi = g; break; }
+  }
+  /* discrete golden-section on [lo, hi] */
+  const double phi = 0.6180339887498949;
+  int32_t a = lo, b = hi;
+  for (int32_t step = 0; b - a > 2 && step < max_steps; ++step) {
+    int32_t x1 = (int32_t)floor(b - phi * (b - a) + 0.5), x2 = (int32_t)floor(a + phi * (b - a) + 0.5);
+    if (x1 <= a) x1 = a + 1;
+    if (x2 >= b) x2 = b - 1;
+    if (x1 >= x2) { /* collision: step one gear toward the larger sub-interval */
+      if (x1 - a >= b - x2) x1 = x2 - 1; else x2 = x1 + 1;
+    }
+    if (x1 <= a || x2 >= b || x1 >= x2) break;
+    if (or_eval(L, x1) < or_eval(L, x2)) b = x2; else a = x1;
+  }
+  if (b - a <= 2)
+    for (int32_t g = a; g <= b; ++g) or_eval(L, g); /* the <= 3 gears left (SPEC: "returns best of the <= 3") */
+  /* least-squares quadratic through the (up to) 5 probes nearest the best probe (normal
+   * equations, centred at the best probe): the search's points around the minimum */
+  int32_t best = -1;
+  for (int32_t g = 0; g < n; ++g)
+    if (L->probed[g] && (best < 0 || L->val[g] < L->val[best])) best = g;
+  int32_t pick[5], m = 0;
+  for (int32_t d = 0; d < n && m < 5; ++d) { /* distance d, lower gear first */
+    if (best - d >= 0 && L->probed[best - d] && m < 5) pick[m++] = best - d;
+    if (d > 0 && best + d < n && L->probed[best + d] && m < 5) pick[m++] = best + d;
+  }
+  int32_t gmin = n, gmax = -1;
+  double S[5] = {0, 0, 0, 0, 0}, Tv[3] = {0, 0, 0};
+  const double c0 = (double)best;
+  for (int32_t i = 0; i < m; ++i) {
+    const int32_t g = pick[i];
+    if (g < gmin) gmin = g;
+    if (g > gmax) gmax = g;
+    const double x = g - c0, v = L->val[g];
+    double xp = 1.0;
+    for (int k = 0; k < 5; ++k) { S[k] += xp; if (k < 3) Tv[k] += xp * v; xp *= x; }
+  }
+  if (m < 3) return best;
+  /* solve [[S4 S3 S2][S3 S2 S1][S2 S1 S0]] (A, B, C) = (T2, T1, T0) by Cramer's rule */
+  const double M[3][3] = {{S[4], S[3], S[2]}, {S[3], S[2], S[1]}, {S[2], S[1], S[0]}};
+  const double r[3] = {Tv[2], Tv[1], Tv[0]};
+  const double det = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) - M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                     M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+  if (!(fabs(det) > 0.0)) return best;
+  const double dA = r[0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) - M[0][1] * (r[1] * M[2][2] - M[1][2] * r[2]) +
+                    M[0][2] * (r[1] * M[2][1] - M[1][1] * r[2]);
+  const double dB = M[0][0] * (r[1] * M[2][2] - M[1][2] * r[2]) - r[0] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                    M[0][2] * (M[1][0] * r[2] - r[1] * M[2][0]);
+  const double A = dA / det, B = dB / det;
+  if (!(A > 0.0)) return best;
+  double gv = c0 - B / (2.0 * A);
+  int32_t g = (int32_t)floor(gv + 0.5);
+  if (g < gmin) g = gmin;
+  if (g > gmax) g = gmax;
+  return g;
+}
+
+int oracle_gear_search(const or_gear_workload* w, const double* sm_mhz, int32_t n_sm, const double* mem_mhz,
+                       int32_t n_mem, double cap, int32_t pred_sm, int32_t pred_mem, or_gear_result* out) {
+  if (n_sm < 1 || n_sm > 256 || n_mem < 1 || n_mem > 256 || pred_sm < 0 || pred_sm >= n_sm || pred_mem < 0 ||
+      pred_mem >= n_mem)
+    return -1;
+  or_line L;
+  memset(&L, 0, sizeof(L));
+  L.w = w; L.sm = sm_mhz; L.mem = mem_mhz; L.n_sm = n_sm; L.n_mem = n_mem; L.cap = cap;
+  L.dom = 1; L.other = pred_sm; /* memory first */
+  const int32_t gm = or_line_search(&L, pred_mem, n_mem);
+  out->probes_mem = L.count;
+  memset(L.probed, 0, sizeof(L.probed));
+  L.count = 0;
+  L.dom = 0; L.other = gm; /* then SM at the chosen memory gear */
+  const int32_t gs = or_line_search(&L, pred_sm, n_sm);
+  out->probes_sm = L.count;
+  out->sm_gear = gs;
+  out->mem_gear = gm;
+  out->objective = oracle_gear_objective(w, sm_mhz, n_sm, mem_mhz, n_mem, cap, gs, gm);
+  return 0;
+}
+int oracle_sizeof_gear(void) { return (int)(sizeof(or_gear_workload) * 1000 + sizeof(or_gear_result)); }
 
 /* O9 (tests only): Err(L) for every L in [L_min, L_max] of an already-formed
  * signal y; returns the global argmin (Err, L). */
