@@ -270,6 +270,30 @@ int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_param
                            int32_t init_samples, gpoeo_measure_result* results, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* ---- Gear local search on a simulated device -------------------------
+ * The online local search of P:585-593, reading R7: memory clock first (at the
+ * predicted SM gear), then SM clock; per domain a bracket from the predicted gear (doubling
+ * strides to a strictly worse value or the boundary), a discrete golden-section search, and a
+ * least-squares quadratic through the probes nearest the best one. The objective comes from
+ * the simulator: T = max(Wc/fs, Wm/fm) + t0, P = Ps + c_sm u_c fs^1.8 + c_mem u_m fm, E = P T,
+ * relative to the highest gears: e + 10 max(0, t - 1 - cap), times (1 + noise h), h in
+ * [-1, 1) a splitmix64 hash of (seed, gears). Batched: one thread per workload. */
+typedef struct {
+  double compute_work, memory_work, overhead, p_static, c_sm, c_mem, u_c, u_m, noise;
+  uint64_t seed;
+} gpoeo_gear_workload; /* 80 bytes */
+
+typedef struct {
+  int32_t sm_gear, mem_gear, probes_sm, probes_mem;
+  double objective;
+} gpoeo_gear_result; /* 24 bytes */
+
+/* workloads, sm_mhz [n_sm] / mem_mhz [n_mem] (ascending, 1..256 gears), pred_sm / pred_mem
+ * [n] and results [n]: DEVICE. Asynchronous, allocation-free. */
+int gpoeo_gear_search(const gpoeo_gear_workload* workloads, int64_t n, const double* sm_mhz, int32_t n_sm,
+                      const double* mem_mhz, int32_t n_mem, double cap, const int32_t* pred_sm,
+                      const int32_t* pred_mem, gpoeo_gear_result* results, void* stream);
+
 /* Work counters of the last device-pointer call that used `workspace` (HOST read after
  * the caller synchronised): number of Alg.2 queries and CEM sample-passes. Used by
  * bench.py to report ALU roofline numbers. Returns GPOEO_OK. */

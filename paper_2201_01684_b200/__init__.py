@@ -53,9 +53,14 @@ ROLLING_DTYPE = np.dtype([("status", "<i4"), ("t_init", "<i4"), ("t_iter", "<i4"
 MEASURE_DTYPE = np.dtype([("status", "<i4"), ("t_iter", "<i4"), ("rounds", "<i4"), ("samples", "<i4"),
                           ("measure_start", "<i4"), ("measure_end", "<i4"), ("t_iter_s", "<f4"), ("err_iter", "<f4")])
 TRACE_UNSTABLE = 4
+GEAR_WORKLOAD_DTYPE = np.dtype([(n, "<f8") for n in ("compute_work", "memory_work", "overhead", "p_static", "c_sm",
+                                                      "c_mem", "u_c", "u_m", "noise")] + [("seed", "<u8")])
+GEAR_RESULT_DTYPE = np.dtype([("sm_gear", "<i4"), ("mem_gear", "<i4"), ("probes_sm", "<i4"), ("probes_mem", "<i4"),
+                              ("objective", "<f8")])
 MAJOR_DTYPE = np.dtype([("period", "<i4"), ("period_s", "<f4"), ("bin", "<i4"), ("status", "<i4")])
 assert RESULT_DTYPE.itemsize == 24 and DETAIL_DTYPE.itemsize == 664 and MAJOR_DTYPE.itemsize == 16
 assert ROLLING_DTYPE.itemsize == 32 and MEASURE_DTYPE.itemsize == 32
+assert GEAR_WORKLOAD_DTYPE.itemsize == 80 and GEAR_RESULT_DTYPE.itemsize == 24
 
 
 class GpoeoRollingParams(ctypes.Structure):
@@ -125,6 +130,9 @@ def load():
     lib.gpoeo_workspace_size_measure.restype = ctypes.c_size_t
     lib.gpoeo_measure_adaptive.argtypes = [P, ctypes.c_int64, PP, RP, ctypes.c_int32, P, P, ctypes.c_size_t, P]
     lib.gpoeo_measure_adaptive.restype = ctypes.c_int
+    lib.gpoeo_gear_search.argtypes = [P, ctypes.c_int64, P, ctypes.c_int32, P, ctypes.c_int32, ctypes.c_double, P, P,
+                                      P, P]
+    lib.gpoeo_gear_search.restype = ctypes.c_int
     lib.gpoeo_read_counters.argtypes = [P, PP, ctypes.c_int64, ctypes.POINTER(GpoeoCounters), P]
     lib.gpoeo_read_counters.restype = ctypes.c_int
     lib.gpoeo_status_string.argtypes = [ctypes.c_int]
@@ -367,6 +375,26 @@ def measure_adaptive(traces, p: GpoeoParams, init_samples: int, rp: GpoeoRolling
                                     ctypes.c_void_p(ws.data_ptr()), ws.numel(), _stream_handle(stream))
     _check(rc, "gpoeo_measure_adaptive")
     return out
+
+
+def gear_search(workloads: np.ndarray, sm_mhz, mem_mhz, cap: float, pred_sm, pred_mem, device="cuda",
+                stream=None) -> np.ndarray:
+    """Gear local search (reading R7) for GEAR_WORKLOAD_DTYPE records on the
+    simulated device, one GPU thread per workload; returns GEAR_RESULT_DTYPE records."""
+    import torch
+    lib = load()
+    n = len(workloads)
+    w = torch.from_numpy(np.ascontiguousarray(workloads).view(np.uint8).copy()).to(device)
+    sm = torch.as_tensor(np.asarray(sm_mhz, np.float64), device=device)
+    mem = torch.as_tensor(np.asarray(mem_mhz, np.float64), device=device)
+    ps = torch.as_tensor(np.asarray(pred_sm, np.int32), device=device)
+    pm = torch.as_tensor(np.asarray(pred_mem, np.int32), device=device)
+    out = torch.empty(n * GEAR_RESULT_DTYPE.itemsize, dtype=torch.uint8, device=device)
+    rc = lib.gpoeo_gear_search(ctypes.c_void_p(w.data_ptr()), n, ctypes.c_void_p(sm.data_ptr()), sm.numel(),
+                               ctypes.c_void_p(mem.data_ptr()), mem.numel(), float(cap), ctypes.c_void_p(ps.data_ptr()),
+                               ctypes.c_void_p(pm.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+    _check(rc, "gpoeo_gear_search")
+    return out.cpu().numpy().view(GEAR_RESULT_DTYPE)
 
 
 def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:

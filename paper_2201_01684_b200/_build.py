@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libgpoeo.so")
-SOURCES = ["gpoeo_api.cu", "composite.cu", "spectrum.cu", "score.cu", "select.cu", "rolling.cu"]
+SOURCES = ["gpoeo_api.cu", "composite.cu", "spectrum.cu", "score.cu", "select.cu", "rolling.cu", "gear.cu"]
 HEADERS = ["gpoeo_internal.cuh"]
 EXTRA = os.environ.get("GPOEO_NVCC_EXTRA", "").split()
 NVCC_FLAGS = EXTRA + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -773,6 +773,19 @@ int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_param
   return GPOEO_OK;
 }
 
+int gpoeo_gear_search(const gpoeo_gear_workload* workloads, int64_t n, const double* sm_mhz, int32_t n_sm,
+                      const double* mem_mhz, int32_t n_mem, double cap, const int32_t* pred_sm,
+                      const int32_t* pred_mem, gpoeo_gear_result* results, void* stream) {
+  if (n < 0 || n_sm < 1 || n_sm > 256 || n_mem < 1 || n_mem > 256 || !(cap >= 0.0))
+    return GPOEO_ERR_INVALID_ARGUMENT;
+  if (n > 0 && (!workloads || !sm_mhz || !mem_mhz || !pred_sm || !pred_mem || !results))
+    return GPOEO_ERR_INVALID_ARGUMENT;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  CK(launch_gear_search(workloads, n, sm_mhz, n_sm, mem_mhz, n_mem, cap, pred_sm, pred_mem, results,
+                        static_cast<cudaStream_t>(stream)));
+  return GPOEO_OK;
+}
+
 size_t gpoeo_similarity_workspace_size(int64_t n_queries) {
   if (n_queries < 0) return 0;
   size_t o = align_up(sizeof(unsigned long long) * kCounterSlots);

@@ -165,6 +165,11 @@ cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, do
                          int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);
 
+// Gear local search (gear.cu)
+cudaError_t launch_gear_search(const gpoeo_gear_workload* w, int64_t n, const double* sm, int32_t n_sm,
+                               const double* mem, int32_t n_mem, double cap, const int32_t* pred_sm,
+                               const int32_t* pred_mem, gpoeo_gear_result* out, cudaStream_t s);
+
 // Alg. 3 (rolling.cu): per-suffix outcome, per-trace suffix plan, parameters
 struct RollSeg {
   int32_t status;

@@ -555,3 +555,36 @@ def test_measure_config2_slice():
 def test_measure_period_shift():
     spec = tg.CFG5.with_(batch=6, n_samples=8192, period_lo=30.0, period_hi=200.0, max_period=2048)
     _measure_compare(tg.generate_host(spec), spec, 2048, "shift")
+
+
+# ---- gear local search (oracle G1, reading R7) ---------------------------
+
+def test_gear_search_matches_oracle():
+    rng = np.random.default_rng(3)
+    sm = np.arange(510, 1966, 15, dtype=np.float64)
+    mem = np.array([405.0, 810.0, 1600.0, 2619.0, 3996.0])
+    n = 400
+    wl = np.zeros(n, dtype=g.GEAR_WORKLOAD_DTYPE)
+    wl["compute_work"] = rng.uniform(0.5e9, 3e9, n)
+    wl["memory_work"] = np.where(rng.random(n) < 0.5, 1e6, rng.uniform(0.5e9, 3e9, n))
+    wl["overhead"] = rng.uniform(0.01, 0.1, n)
+    wl["p_static"] = rng.uniform(60, 150, n)
+    wl["c_sm"] = rng.uniform(2e-4, 1e-3, n)
+    wl["c_mem"] = rng.uniform(0.005, 0.03, n)
+    wl["u_c"] = rng.uniform(0.2, 1.0, n)
+    wl["u_m"] = rng.uniform(0.2, 1.0, n)
+    wl["noise"] = np.where(rng.random(n) < 0.5, 0.0, 0.01)
+    wl["seed"] = rng.integers(0, 1 << 62, n, dtype=np.uint64)
+    ps = rng.integers(0, len(sm), n).astype(np.int32)
+    pm = rng.integers(0, len(mem), n).astype(np.int32)
+    r = g.gear_search(wl, sm, mem, 0.05, ps, pm)
+    bad = 0
+    for i in range(n):
+        w = O.gear_workload(**{k: (int(wl[k][i]) if k == "seed" else float(wl[k][i])) for k in wl.dtype.names})
+        o = O.gear_search(w, sm, mem, 0.05, int(ps[i]), int(pm[i]))
+        got = (int(r[i]["sm_gear"]), int(r[i]["mem_gear"]), int(r[i]["probes_sm"]), int(r[i]["probes_mem"]))
+        if got != (o["sm_gear"], o["mem_gear"], o["probes_sm"], o["probes_mem"]):
+            bad += 1  # only a last-ulp difference of pow() between the two libraries can do this
+            continue
+        assert abs(r[i]["objective"] - o["objective"]) <= 1e-12 * abs(o["objective"])
+    assert bad <= 2, bad
