@@ -356,6 +356,54 @@ def run_gpu(args) -> None:
             "stable_frac": float((mr["status"] == 0).mean()),
             "timing": "wall clock of the synchronous gpoeo_measure_adaptive (recordings resident in HBM)"}
 
+    # gear local search over simulated workloads: one thread per workload
+    if not args.no_rolling:
+        import numpy as np
+        rng = np.random.default_rng(11)
+        ng = args.gear_workloads
+        wl = np.zeros(ng, dtype=g.GEAR_WORKLOAD_DTYPE)
+        wl["compute_work"] = rng.uniform(0.5e9, 3e9, ng)
+        wl["memory_work"] = rng.uniform(0.5e9, 3e9, ng)
+        wl["overhead"] = rng.uniform(0.01, 0.1, ng)
+        wl["p_static"] = rng.uniform(60, 150, ng)
+        wl["c_sm"] = rng.uniform(2e-4, 1e-3, ng)
+        wl["c_mem"] = rng.uniform(0.005, 0.03, ng)
+        wl["u_c"] = rng.uniform(0.2, 1.0, ng)
+        wl["u_m"] = rng.uniform(0.2, 1.0, ng)
+        wl["noise"] = 0.01
+        wl["seed"] = rng.integers(0, 1 << 62, ng, dtype=np.uint64)
+        smg = np.arange(510, 1966, 15, dtype=np.float64)
+        memg = np.array([405.0, 810.0, 1600.0, 2619.0, 3996.0])
+        dwl = torch.from_numpy(wl.view(np.uint8).copy()).to(dev)
+        dsm, dmem = torch.as_tensor(smg, device=dev), torch.as_tensor(memg, device=dev)
+        dps = torch.as_tensor(rng.integers(0, len(smg), ng).astype(np.int32), device=dev)
+        dpm = torch.as_tensor(rng.integers(0, len(memg), ng).astype(np.int32), device=dev)
+        dout = torch.empty(ng * g.GEAR_RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        lib = g.load()
+        import ctypes as _ct
+
+        def _gear():
+            rc = lib.gpoeo_gear_search(_ct.c_void_p(dwl.data_ptr()), ng, _ct.c_void_p(dsm.data_ptr()), len(smg),
+                                       _ct.c_void_p(dmem.data_ptr()), len(memg), 0.05, _ct.c_void_p(dps.data_ptr()),
+                                       _ct.c_void_p(dpm.data_ptr()), _ct.c_void_p(dout.data_ptr()),
+                                       _ct.c_void_p(stream.cuda_stream))
+            assert rc == 0
+        _gear()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            _gear()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = _max_over_ranks(g0.elapsed_time(g1), dev) / args.steps
+        gr = dout.cpu().numpy().view(g.GEAR_RESULT_DTYPE)
+        line["gear_search"] = {
+            "metric": "workloads/sec gear local search (P:585-593) on the simulated device", "value": world * ng / (gms / 1e3),
+            "unit": "workloads/s", "workloads_per_gpu": ng, "ms_per_step": gms,
+            "mean_probes_sm": float(gr["probes_sm"].mean()), "mean_probes_mem": float(gr["probes_mem"].mean()),
+            "gears": f"{len(smg)} SM x {len(memg)} memory", "note": "control logic, one thread per workload"}
+
     # e2e: same metric through the public host entry point (pinned host buffers, H2D+D2H inside)
     del x
     torch.cuda.empty_cache()
@@ -421,6 +469,7 @@ def main():
     ap.add_argument("--no-rolling", action="store_true")
     ap.add_argument("--rolling-batch", type=int, default=5000)
     ap.add_argument("--rolling-steps", type=int, default=2)
+    ap.add_argument("--gear-workloads", type=int, default=100_000)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
