@@ -140,6 +140,8 @@ struct PeakShared {
   int32_t sorted[kPeakCap];
   float redP[32];
   int32_t redk[32];
+  float pm[8];    // per-rank in-band peak maximum (cluster kernels)
+  int32_t pk[8];  // its bin
   int32_t count;
   int32_t overflow;
 };
@@ -357,6 +359,13 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
   const float2* z = reinterpret_cast<const float2*>(y + t * p.ystride);
 
   // ---- load + DIF split across the cluster: a_q[j2] -------------------------------
+  float2 wq[C];  // W_C^((r q) mod C), fixed per CTA
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    float s, c;
+    sincospif(-2.0f * (float)((r * q) % C) / (float)C, &s, &c);
+    wq[r] = make_float2(c, s);
+  }
   for (int j2 = threadIdx.x; j2 < n2; j2 += T) {
     float2 acc;
     if constexpr (C == 1) {
@@ -364,12 +373,7 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
     } else {
       acc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int r = 0; r < C; ++r) {
-        float2 v = __ldg(z + j2 + r * n2);
-        float s, c;
-        sincospif(-2.0f * (float)((r * q) % C) / (float)C, &s, &c);
-        acc = cadd(acc, cmul(v, make_float2(c, s)));
-      }
+      for (int r = 0; r < C; ++r) acc = cadd(acc, cmul(__ldg(z + j2 + r * n2), wq[r]));
       if (q) {
         float s, c;
         sincospif(-2.0f * (float)(j2 * q) / (float)n, &s, &c);
@@ -438,19 +442,88 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
     __syncthreads();
   }
 
-  // ---- peaks -> candidates (cluster rank 0) ------------------------------------------
-  if (mode != kPeaksNone && q == 0) {
+  // ---- peaks -> candidates ------------------------------------------------------------
+  if constexpr (C == 1) {
+    if (mode != kPeaksNone) {
+      PView<1> Pv;
+      Pv.n = n;
+      Pv.base[0] = P;
+      if (mode == kPeaksMajor) find_major<PView<1>, T>(p, Pv, t, status_in[t], w.major, ps);
+      else find_candidates<PView<1>, T>(p, Pv, t, status_in[t], w, ps);
+    }
+  } else if (mode != kPeaksNone) {
+    // every CTA tests its own bins k = C k2 + q (neighbours through DSMEM); the in-band
+    // maximum is combined on every rank, the candidates collected on rank 0
+    cg::cluster_group cluster = cg::this_cluster();
     PView<C> Pv;
     Pv.n = n;
-    if constexpr (C > 1) {
-      cg::cluster_group cluster = cg::this_cluster();
 #pragma unroll
-      for (int r = 0; r < C; ++r) Pv.base[r] = cluster.map_shared_rank(P, r);
-    } else {
-      Pv.base[0] = P;
+    for (int r = 0; r < C; ++r) Pv.base[r] = cluster.map_shared_rank(P, r);
+    PeakShared* ps0 = cluster.map_shared_rank(&ps, 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k2lo = (p.k_lo - q + C - 1) / C, k2hi = p.k_hi >= q ? (p.k_hi - q) / C : -1;
+    float bp = -1.f;
+    int32_t bk = 0x7fffffff;
+    for (int k2 = k2lo + threadIdx.x; k2 <= k2hi; k2 += T) {
+      const int64_t k = (int64_t)C * k2 + q;
+      const float pk = P[k2];
+      if (pk > bp && pk > Pv(k - 1) && pk >= Pv(k + 1)) { bp = pk; bk = (int32_t)k; }
     }
-    if (mode == kPeaksMajor) find_major<PView<C>, T>(p, Pv, t, status_in[t], w.major, ps);
-    else find_candidates<PView<C>, T>(p, Pv, t, status_in[t], w, ps);
+    for (int off = 16; off; off >>= 1) {
+      const float op = __shfl_xor_sync(0xffffffffu, bp, off);
+      const int32_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+      if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+    }
+    if (lane == 0) { ps.redP[warp] = bp; ps.redk[warp] = bk; }
+    __syncthreads();
+    if (threadIdx.x < C) {  // my CTA's best to every rank, slot q
+      for (int i = 1; i < T / 32; ++i) {
+        const float op = ps.redP[i];
+        const int32_t ok = ps.redk[i];
+        if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
+      }
+      PeakShared* pr = cluster.map_shared_rank(&ps, (int)threadIdx.x);
+      pr->pm[q] = bp;
+      pr->pk[q] = bk;
+    }
+    if (q == 0 && threadIdx.x == 0) ps.count = 0;
+    cluster.sync();
+    float pmax = -1.f;
+    int32_t kmax = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < C; ++r)
+      if (ps.pm[r] > pmax || (ps.pm[r] == pmax && ps.pk[r] < kmax)) { pmax = ps.pm[r]; kmax = ps.pk[r]; }
+    const int32_t st = status_in[t];
+    if (mode == kPeaksMajor) {
+      if (q == 0 && threadIdx.x == 0) {
+        int32_t status = st;
+        if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;
+        if (status == GPOEO_TRACE_OK && pmax < 0.f) status = GPOEO_TRACE_APERIODIC;
+        gpoeo_major_result r;
+        r.status = status;
+        r.bin = status == GPOEO_TRACE_OK ? kmax : -1;
+        r.period = status == GPOEO_TRACE_OK ? p.N / kmax : -1;
+        r.period_s = status == GPOEO_TRACE_OK ? (float)((double)r.period * p.Ts) : -1.f;
+        w.major[t] = r;
+      }
+    } else {
+      const double thr = (double)p.c_peak * (double)p.c_peak * (double)pmax;
+      if (pmax >= 0.f) {
+        for (int k2 = k2lo + threadIdx.x; k2 <= k2hi; k2 += T) {
+          const int64_t k = (int64_t)C * k2 + q;
+          const float pk = P[k2];
+          if ((double)pk > thr && pk > Pv(k - 1) && pk >= Pv(k + 1)) {
+            const int slot = atomicAdd(&ps0->count, 1);
+            if (slot < kPeakCap) {
+              ps0->pk_P[slot] = pk;
+              ps0->pk_k[slot] = (int32_t)k;
+            }
+          }
+        }
+      }
+      cluster.sync();
+      if (q == 0) finish_candidates<PView<C>, T>(p, Pv, t, st, w, ps, pmax);
+    }
   }
   if constexpr (C > 1) cg::this_cluster().sync();  // keep our P alive while rank 0 reads it
 }
