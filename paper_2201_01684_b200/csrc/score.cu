@@ -39,7 +39,8 @@ constexpr unsigned FULL = 0xffffffffu;
 
 #ifdef GPOEO_STATS
 // debug build only: [0] bucket pairs, [1] bucket passes, [2] members swept (straddling +
-// relabelled), [3] straddling members, [4] straddling buckets, [5] team pairs, [6] team passes
+// relabelled), [3] straddling members, [4] straddling buckets, [5] team pairs, [6] team passes,
+// [7] team-kernel warp pass iterations
 __device__ unsigned long long g_stats[16];
 #define GPOEO_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 // [8..11]: bucket-path cycles of lane 0 in (range + counting sort), bucket sums, CEM passes, final
@@ -286,6 +287,7 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
   int passes = 0;
   for (int it = 1; it <= maxit; ++it) {
     if (!__any_sync(FULL, active)) break;
+    if (lane == 0) GPOEO_STAT(7, 1);  // warp pass iterations (debug: lane utilisation of teams)
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;

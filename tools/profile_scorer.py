@@ -60,7 +60,8 @@ def main():
                             "swept_members_per_pass": s[2] / max(s[1], 1),
                             "straddle_members_per_pass": s[3] / max(s[1], 1),
                             "straddle_buckets_per_pass": s[4] / max(s[1], 1), "team_pairs": s[5],
-                            "team_passes_per_pair": s[6] / max(s[5], 1),
+                            "team_passes_per_pair": s[6] / max(s[5], 1), "team_warp_iterations": s[7],
+                            "team_pair_passes": s[6],
                             "bucket_cycles_per_pair": {k: s[8 + i] / max(s[0], 1) for i, k in
                                                        enumerate(["range_sort", "bucket_sums", "passes", "final"])}}
     out["counters"] = g.read_counters(ws, p, args.batch)
