@@ -156,7 +156,9 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
 /* Debug/parity surface mirroring fft_spectrum: composite signal (Z1) and its
  * unnormalised power spectrum P[k] = |X_k|^2, k = 0..N/2 (Alg.1 l.1-2, Z2-Z4).
  *  spectra [batch][N/2+1] fp32 (may be NULL), signal [batch][N] fp32 (may be NULL).
- * Same workspace rules as gpoeo_detect_periods. */
+ * Same workspace rules as gpoeo_detect_periods. For N not a power of two every bin is
+ * evaluated by the DFT definition and held in shared memory: spectra need N/2 + 1 <= ~50K
+ * (else GPOEO_ERR_UNSUPPORTED). */
 int gpoeo_power_spectrum(const float* traces, int64_t batch, const gpoeo_params* p, float* spectra, float* signal,
                          void* workspace, size_t workspace_bytes, void* stream);
 
