@@ -783,14 +783,28 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       }
       __syncwarp();
       int fcur = 0;  // g grows by 32 per trip: walk the (offset-sorted) flags forward
-#pragma unroll 1
-      for (int g = lane; g < total; g += 32) {
+      // member g -> (bucket, position); the gather of the next member is issued before the
+      // current one is evaluated (one load in flight behind the fp64 work)
+      auto locate = [&](int g, int& b, int& p) {
         while (fcur + 1 < nfl && (int)(bv.flag[fcur + 1] >> 8) <= g) ++fcur;
         const uint32_t f = bv.flag[fcur];
-        const int b = (int)(f & 0xFFu);
-        const int i = bv.off[b] + (g - (int)(f >> 8));
-        const int p = bv.pos[i];
-        const double y = (double)__ldg(A + p);
+        b = (int)(f & 0xFFu);
+        p = bv.pos[bv.off[b] + (g - (int)(f >> 8))];
+      };
+      int bn = 0, pn = 0;
+      float yn = 0.f;
+      if (lane < total) {
+        locate(lane, bn, pn);
+        yn = __ldg(A + pn);
+      }
+#pragma unroll 1
+      for (int g = lane; g < total; g += 32) {
+        const int b = bn, p = pn;
+        const double y = (double)yn;
+        if (g + 32 < total) {
+          locate(g + 32, bn, pn);
+          yn = __ldg(A + pn);
+        }
         double e[G];
         const int lbl = cem.assign(y, it, e);
 #pragma unroll
