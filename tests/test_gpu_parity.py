@@ -588,3 +588,28 @@ def test_gear_search_matches_oracle():
             continue
         assert abs(r[i]["objective"] - o["objective"]) <= 1e-12 * abs(o["objective"])
     assert bad <= 2, bad
+
+
+def test_rolling_and_measure_non_pow2_weighted():
+    # N not a power of two, three channels with unequal weights (Z1): Alg. 3 and Alg. 4
+    spec = tg.CFG2.with_(batch=8, n_samples=3000, period_lo=20.0, period_hi=300.0, min_period=10, max_period=1000)
+    x = tg.generate_host(spec)
+    w = (1.0, 0.5, 2.0)
+    p = g.params_for(spec)
+    for c, v in enumerate(w):
+        p.feature_weights[c] = v
+    r = g.detect_rolling(_to_dev(x), p)
+    op = O.params_for(spec, dft_band_only=True, weights=w)
+    agree = 0
+    for i in range(x.shape[0]):
+        o = O.rolling(x[i], op)
+        agree += (r[i]["status"], r[i]["t_init"], r[i]["t_iter"], r[i]["n_sub"]) == (o.status, o.t_init, o.t_iter,
+                                                                                    len(o.sub_start))
+    assert agree >= x.shape[0] - 1
+    m = g.measure_adaptive(_to_dev(x), p, 600)
+    agree = 0
+    for i in range(x.shape[0]):
+        o = O.measure(x[i], op, 600)
+        agree += (int(m[i]["t_iter"]), int(m[i]["rounds"]), int(m[i]["samples"])) == (o["t_iter"], o["rounds"],
+                                                                                       o["samples"])
+    assert agree >= x.shape[0] - 1
