@@ -408,7 +408,8 @@ def run_gpu(args) -> None:
     del x
     torch.cuda.empty_cache()
     if not args.no_e2e:
-        Be = min(args.e2e_batch, B)
+        # pinned host memory is shared by the ranks of the box: 8192 traces (6.4 GB) per rank at N > 1
+        Be = min(args.e2e_batch, B) if world == 1 else min(args.e2e_batch, B, 8192)
         xh = torch.empty((Be, spec.n_features * spec.n_samples), dtype=torch.float32, pin_memory=True)
         tmp = torch.empty((min(Be, 4096), spec.n_features * spec.n_samples), dtype=torch.float32, device=dev)
         for i0 in range(0, Be, tmp.shape[0]):
