@@ -5,7 +5,7 @@
         python tools/profile_scorer.py --batch B --repeat 1
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --csv --log-file S.csv \\
         python tools/profile_spectral.py --batch B --steps 1 --warmup 0
-    python tools/ncu_traffic.py A.csv S.csv B
+    python tools/ncu_traffic.py A.csv S.csv B [OUT.json]   (default profiles/ncu_traffic.json)
 
 DRAM bytes (read + write) per trace of the Alg. 2 scorer kernels (every score_* launch of
 the first detect call) and of the spectral-only fused kernel.
@@ -56,7 +56,7 @@ def main():
                 "spectral-only mode per trace (algorithmic 786448 B)",
         "launches": [{"kernel": n[:80], "dram_bytes": b} for n, b in first],
     }
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    path = sys.argv[4] if len(sys.argv) > 4 else os.path.join(ROOT, "profiles", "ncu_traffic.json")
     json.dump(out, open(path, "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "launches"}))
 
