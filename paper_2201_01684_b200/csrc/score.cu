@@ -404,10 +404,17 @@ constexpr int kBucketMaxL = 8192;
 constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order (the range carry needs it)
 static_assert(kBucketWarps == 1, "pair_err_bucket's range carry assumes one warp walks a query's pairs in order");
 
+// lab[] and the counting sort's lcnt[] share one area: lcnt is dead once the sort is done,
+// and lab[p] is read only for members of a mixed bucket, all written by the sweep that
+// made it mixed (a smaller region leaves more of the SM's unified L1 for the gathers)
+__host__ __device__ constexpr size_t bucket_labcnt_bytes(int Lcap) {
+  return (((size_t)Lcap + 15) & ~(size_t)15) > (size_t)kBuckets * 32 * 2 ? (((size_t)Lcap + 15) & ~(size_t)15)
+                                                                          : (size_t)kBuckets * 32 * 2;
+}
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
-  return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + (((size_t)Lcap + 15) & ~(size_t)15) + (size_t)kBuckets * 8 * 2 +
-         (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 2 + (size_t)kBuckets * 4 +
-         (size_t)kBuckets * 32 * 2 + kBuckets + (size_t)kBuckets * 4 + 64;
+  return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + bucket_labcnt_bytes(Lcap) + (size_t)kBuckets * 8 * 2 +
+         (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 4 + kBuckets +
+         (size_t)kBuckets * 4 + 64;
 }
 
 struct BucketView {
@@ -419,9 +426,8 @@ struct BucketView {
   float* bmax;     // [K]
   float* cb;       // [K]   shift (first member's value)
   uint16_t* off;   // [K+1] first slot of bucket b
-  uint16_t* cur;   // [K]   scatter cursors
   uint32_t* flag;  // [K]   flagged-bucket list of a pass: (member offset << 8) | bucket
-  uint16_t* lcnt;  // [K][32] per-lane bucket counts / scatter cursors of the counting sort
+  uint16_t* lcnt;  // [K][32] per-lane bucket counts / scatter cursors of the counting sort (aliases lab)
   uint8_t* blab;   // [K]   bucket state: l < G every member has label l; 0xFF mixed (lab[]); 0xFE unset
   uint32_t* seen;  // [K]   labels seen among a straddling bucket's members this pass (bit mask)
 
@@ -431,7 +437,8 @@ struct BucketView {
     v.pos = reinterpret_cast<uint16_t*>(p);
     p += ((size_t)Lcap * 2 + 15) & ~(size_t)15;
     v.lab = p;
-    p += ((size_t)Lcap + 15) & ~(size_t)15;
+    v.lcnt = reinterpret_cast<uint16_t*>(p);
+    p += bucket_labcnt_bytes(Lcap);
     v.s1 = reinterpret_cast<double*>(p);
     p += (size_t)kBuckets * 8;
     v.s2 = reinterpret_cast<double*>(p);
@@ -444,12 +451,8 @@ struct BucketView {
     p += (size_t)kBuckets * 4;
     v.off = reinterpret_cast<uint16_t*>(p);
     p += (size_t)(kBuckets + 8) * 2;
-    v.cur = reinterpret_cast<uint16_t*>(p);
-    p += (size_t)kBuckets * 2;
     v.flag = reinterpret_cast<uint32_t*>(p);
     p += (size_t)kBuckets * 4;
-    v.lcnt = reinterpret_cast<uint16_t*>(p);
-    p += (size_t)kBuckets * 32 * 2;
     v.blab = p;
     p += ((size_t)kBuckets + 3) & ~(size_t)3;
     v.seen = reinterpret_cast<uint32_t*>(p);
