@@ -225,6 +225,95 @@ __device__ __forceinline__ void mstep(Cem<G>& cem, const double* v, int L, int t
   }
 }
 
+#ifndef GPOEO_TEAM_RS
+#define GPOEO_TEAM_RS 1
+#endif
+// Recursive-halving team reduction of the 2G pass sums + M-step (sub-warp and warp teams
+// of tau >= pow2ceil(2G) lanes). The counts go two per 32-bit word by butterfly (n_j <= L
+// < 2^16), "any label changed" as a ballot over the team's lanes; the 2G doubles (S_j at
+// index j, Q_j at index G + j) by H = log2(pow2ceil(2G)) halving steps, after which team
+// lane lt holds index k = lt >> (log2 tau - H) (2^(log2 tau - H) lanes each, finished by a
+// butterfly): H fewer shuffle rounds of all 2G values than the full butterfly. Component j
+// is updated on the lanes holding S_j and broadcast from the first of them.
+template <int G>
+__host__ __device__ constexpr int team_rs_h() {
+  return 2 * G <= 2 ? 1 : (2 * G <= 4 ? 2 : (2 * G <= 8 ? 3 : 4));
+}
+template <int G>
+__host__ __device__ constexpr int team_rs_min() {
+  return 1 << team_rs_h<G>();
+}
+template <int G>
+__device__ __forceinline__ void team_reduce_mstep(Cem<G>& cem, const double* v, const int32_t* n, int changed,
+                                                  bool& active, int& passes, int it, int maxit, int L, int tau,
+                                                  int lane) {
+  constexpr int H = team_rs_h<G>();
+  constexpr int NVR = 1 << H;
+  constexpr int NPK = (G + 1) / 2;
+  const int base = lane & ~(tau - 1);
+  const int lt = lane - base;
+  const unsigned tmask = tau == 32 ? FULL : (((1u << tau) - 1u) << base);
+  const bool tchanged = (__ballot_sync(FULL, changed) & tmask) != 0u;
+  if (active) {
+    passes = it;
+    if ((it > 1 && !tchanged) || it == maxit) active = false;  // labels final
+  }
+  if (!__any_sync(FULL, active)) return;  // no team of the warp needs a new model
+  unsigned pk[NPK];
+#pragma unroll
+  for (int i = 0; i < NPK; ++i) pk[i] = (unsigned)n[2 * i] | ((2 * i + 1 < G ? (unsigned)n[2 * i + 1] : 0u) << 16);
+#pragma unroll 1
+  for (int off = tau >> 1; off; off >>= 1) {
+#pragma unroll
+    for (int i = 0; i < NPK; ++i) pk[i] += __shfl_xor_sync(FULL, pk[i], off);
+  }
+  double rs[NVR];
+#pragma unroll
+  for (int k = 0; k < NVR; ++k) rs[k] = k < 2 * G ? v[G + k] : 0.0;
+#pragma unroll
+  for (int hl = 0; hl < H; ++hl) {
+    const int off = tau >> (hl + 1);
+    const bool up = (lane & off) != 0;
+    const int half = NVR >> (hl + 1);
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = up ? rs[i] : rs[i + half];
+      const double keep = up ? rs[i + half] : rs[i];
+      rs[i] = keep + __shfl_xor_sync(FULL, send, off);
+    }
+  }
+#pragma unroll 1
+  for (int off = tau >> (H + 1); off; off >>= 1) rs[0] += __shfl_xor_sync(FULL, rs[0], off);
+  const int sh = (31 - __clz(tau)) - H;
+  const int j = lt >> sh;
+  const double Q = __shfl_sync(FULL, rs[0], base + (j < G ? ((G + j) << sh) : lt));
+  double mu = 0.0, c = -INFINITY, h = 0.0;
+  if (j < G) {
+    double nj = 0.0;
+#pragma unroll
+    for (int k = 0; k < G; ++k)
+      if (k == j) { nj = (double)((pk[k / 2] >> (16 * (k & 1))) & 0xFFFFu); mu = cem.mu[k]; }
+    if (nj != 0.0) {  // empty: dead (stays dead)
+      const double rn = rcp_fast(nj);
+      const double m = rs[0] * rn;
+      const double dm = m - mu;
+      double var = Q * rn - dm * dm;
+      if (var < cem.floor_var) var = cem.floor_var;
+      h = 0.5 * rcp_fast(var);
+      const double pp = nj * (1.0 / (double)L);
+      mu = m;
+      c = 0.5 * log(2.0 * pp * pp * h);  // ln pi - 1/2 ln var
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int src = base + (k << sh);
+    cem.mu[k] = __shfl_sync(FULL, mu, src);
+    cem.c[k] = __shfl_sync(FULL, c, src);
+    cem.h[k] = __shfl_sync(FULL, h, src);
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // One pair, samples resident in shared memory. Lane lt of the team owns samples
 // s = lt + u*tau, u < cnt, stored at ys[u * kScoreThreads] (conflict-free: consecutive
@@ -291,11 +380,11 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;
-    if (active) {
-      int32_t n[G];
-      int changed = 0;
+    int32_t n[G];
+    int changed = 0;
 #pragma unroll
-      for (int j = 0; j < G; ++j) n[j] = 0;
+    for (int j = 0; j < G; ++j) n[j] = 0;
+    if (active) {
       if (it == 1) {
 #pragma unroll 1
         for (int u = 0; u < cnt; ++u) {
@@ -322,6 +411,14 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
             if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
         }
       }
+    }
+#if GPOEO_TEAM_RS
+    if (tau >= team_rs_min<G>() && tau <= 32) {  // warp-uniform (one query per CTA)
+      team_reduce_mstep<G>(cem, v, n, changed, active, passes, it, maxit, L, tau, lane);
+      continue;
+    }
+#endif
+    if (active) {
 #pragma unroll
       for (int j = 0; j < G; ++j) v[j] = (double)n[j];
       v[3 * G] = (double)changed;
@@ -402,6 +499,9 @@ static_assert((kBuckets <= 32 || kBuckets % 32 == 0) && kBuckets <= 255,
               "a lane owns kBuckets/32 whole buckets; the flag word keeps the bucket in 8 bits");
 constexpr int kBucketMaxL = 8192;
 constexpr int kBucketWarps = 1;  // bucket-kernel CTA = one warp: a query's pairs in order (the range carry needs it)
+#ifndef GPOEO_BUCKET_RS
+#define GPOEO_BUCKET_RS 1
+#endif
 static_assert(kBucketWarps == 1, "pair_err_bucket's range carry assumes one warp walks a query's pairs in order");
 
 // lab[] and the counting sort's lcnt[] share one area: lcnt is dead once the sort is done,
@@ -831,8 +931,15 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     }
     __syncwarp();
     passes = it;
-    // warp sums: S_j, Q_j as doubles; the counts two per 32-bit word (n_j <= L < 2^16);
-    // "any label changed" as a vote
+#if GPOEO_BUCKET_RS
+    // the last pass needs no sums (the final pass below recomputes the groups' statistics)
+    bool act = true;
+    team_reduce_mstep<G>(cem, v, nc, changed, act, passes, it, maxit, L, 32, lane);
+    if (!act) break;  // labels final
+#else
+    const bool any_changed = __any_sync(FULL, changed);
+    if ((it > 1 && !any_changed) || it == maxit) break;  // labels final
+    // warp sums: S_j, Q_j as doubles; the counts two per 32-bit word (n_j <= L < 2^16)
     {
       constexpr int NPK = (G + 1) / 2;
       unsigned pk[NPK];
@@ -848,9 +955,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
 #pragma unroll
       for (int j = 0; j < G; ++j) v[j] = (double)((pk[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
     }
-    const bool any_changed = __any_sync(FULL, changed);
-    if ((it > 1 && !any_changed) || it == maxit) break;  // labels final
     mstep<G>(cem, v, L, 32, lane);
+#endif
   }
   if (lane == 0) { GPOEO_STAT(0, 1); GPOEO_STAT(1, passes); }
   GPOEO_TICK(10, tk);
