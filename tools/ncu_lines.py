@@ -1,7 +1,9 @@
 #!/usr/bin/env python
 """Aggregate an ncu source page (SASS) per CUDA source line (profiling helper).
 
-    python tools/ncu_lines.py gpurun_out/bucket.ncu-rep score_bucket_kernel [lib.so] [--top 40]
+    python tools/ncu_lines.py gpurun_out/bucket.ncu-rep score_bucket_kernel [lib.so] [--top 40] [--section I]
+
+(--section I: the I-th "Kernel Name" block of the source page, for reports of several launches)
 
 Maps each SASS offset of the kernel to its source line with `nvdisasm -g` on the cubin
 extracted from the library (built with -lineinfo), then sums "Instructions Executed"
@@ -59,6 +61,10 @@ def main():
     txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
+    if "--section" in sys.argv:  # reports with several launches: the I-th "Kernel Name" block
+        want = int(sys.argv[sys.argv.index("--section") + 1])
+        starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+        rows = rows[starts[want]:starts[want + 1]]
     hdr = rows[1]
     ia, ie, ist = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index(
         "Warp Stall Sampling (All Samples)")
