@@ -6,6 +6,7 @@
 //   memset(counters) -> composite (a1) -> spectrum+peaks (a2, a3; appends candidate
 //   queries) -> score(candidate queries) (a4) -> select (a5, a6; appends local queries)
 //   -> score(local queries) (a4) -> final (a7).
+#include <algorithm>
 #include <math.h>
 #include <stdio.h>
 #include <string.h>
@@ -522,14 +523,23 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
   cudaEventRecord(start, s);
   cudaStreamWaitEvent(cs, start, 0);
   cudaStreamWaitEvent(s2, start, 0);
-  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  // chunk boundaries: the first two chunks ramp up (chunk/4, chunk/2) so compute starts after
+  // a quarter of the first full copy instead of all of it; then full chunks
+  std::vector<int64_t> cfirst;
+  for (int64_t first = 0, c = 0; first < batch; ++c) {
+    cfirst.push_back(first);
+    const int64_t sz = c < 2 ? std::max<int64_t>(chunk >> (2 - c), 1) : chunk;
+    first += sz;
+  }
+  cfirst.push_back(batch);
+  const int64_t nchunks = (int64_t)cfirst.size() - 1;
   // results of chunk c leave through the copy stream when buffer c % 3 is reused (or at the
   // end): a D2H copy into pageable host memory blocks the host until it completes, so it is
   // issued three chunks late, while the two chunks after it keep the GPU busy
   auto drain = [&](int64_t c) -> int {
     const int b = (int)(c % kHostBuffers);
-    const int64_t first = c * chunk;
-    const int64_t n = batch - first < chunk ? batch - first : chunk;
+    const int64_t first = cfirst[c];
+    const int64_t n = cfirst[c + 1] - first;
     if (cudaStreamWaitEvent(cs, done[b], 0) != cudaSuccess) return GPOEO_ERR_CUDA;
     if (cudaMemcpyAsync(host_results + first, dres[b], sizeof(gpoeo_result) * n, cudaMemcpyDeviceToHost, cs) !=
         cudaSuccess)
@@ -539,8 +549,8 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
   for (int64_t c = 0; c < nchunks && rc == GPOEO_OK; ++c) {
     const int b = (int)(c % kHostBuffers);
     cudaStream_t cstr = cst[c & 1];
-    const int64_t first = c * chunk;
-    const int64_t n = batch - first < chunk ? batch - first : chunk;
+    const int64_t first = cfirst[c];
+    const int64_t n = cfirst[c + 1] - first;
     if (c >= kHostBuffers) rc = drain(c - kHostBuffers);  // buffer b free again once drained
     if (rc == GPOEO_OK &&
         cudaMemcpyAsync(dtr[b], host_traces + first * p->trace_stride, sizeof(float) * (size_t)p->trace_stride * n,
