@@ -40,8 +40,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifdef GPOEO_STATS
 // debug build only: [0] bucket pairs, [1] bucket passes, [2] members swept (straddling +
 // relabelled), [3] straddling members, [4] straddling buckets, [5] team pairs, [6] team passes,
-// [7] team-kernel warp pass iterations
-__device__ unsigned long long g_stats[16];
+// [7] team-kernel warp pass iterations; [12..15] those by team width class (tau = 1, 2-4,
+// 8-16, >= 32), [16..19] team pair passes by class, [20..23] team pairs by class
+__device__ unsigned long long g_stats[24];
 #define GPOEO_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 // [8..11]: bucket-path cycles of lane 0 in (range + counting sort), bucket sums, CEM passes, final
 #define GPOEO_TICK(i, t0)                                  \
@@ -377,6 +378,7 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
   for (int it = 1; it <= maxit; ++it) {
     if (!__any_sync(FULL, active)) break;
     if (lane == 0) GPOEO_STAT(7, 1);  // warp pass iterations (debug: lane utilisation of teams)
+    if (lane == 0) GPOEO_STAT(12 + (tau == 1 ? 0 : tau <= 4 ? 1 : tau <= 16 ? 2 : 3), 1);
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = 0.0;
@@ -456,6 +458,10 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
   team_allreduce<NV>(v, tau, team, lane, warp, red, buf);
   if (!clustered) return 0.0;
   if (lt == 0) { passes_out += (long long)(passes + 1) * L; GPOEO_STAT(5, 1); GPOEO_STAT(6, passes); }
+  if (lt == 0) {
+    GPOEO_STAT(16 + (tau == 1 ? 0 : tau <= 4 ? 1 : tau <= 16 ? 2 : 3), passes);
+    GPOEO_STAT(20 + (tau == 1 ? 0 : tau <= 4 ? 1 : tau <= 16 ? 2 : 3), 1);
+  }
   const double mA = TA / (double)L, mB = v[3 * G] / (double)L;
   double num = 0.0;
 #pragma unroll
@@ -1334,9 +1340,9 @@ cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, do
 
 #ifdef GPOEO_STATS
 extern "C" __attribute__((visibility("default"))) int gpoeo_debug_stats(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, gpoeo::g_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return -5;
+  if (cudaMemcpyFromSymbol(out, gpoeo::g_stats, sizeof(unsigned long long) * 24) != cudaSuccess) return -5;
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[24] = {0};
     cudaMemcpyToSymbol(gpoeo::g_stats, z, sizeof(z));
   }
   return 0;

@@ -43,7 +43,7 @@ def main():
     out = {}
     for r in range(args.repeat):
         if stats_fn is not None:
-            buf = (ctypes.c_ulonglong * 16)()
+            buf = (ctypes.c_ulonglong * 24)()
             stats_fn(buf, 1)
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         for e in evs:
@@ -53,7 +53,7 @@ def main():
         torch.cuda.synchronize()
         out["phase_ms"] = {n: evs[i].elapsed_time(evs[i + 1]) for i, n in enumerate(g.PHASES)}
         if stats_fn is not None:
-            buf = (ctypes.c_ulonglong * 16)()
+            buf = (ctypes.c_ulonglong * 24)()
             stats_fn(buf, 0)
             s = list(buf)
             out["stats"] = {"bucket_pairs": s[0], "bucket_passes_per_pair": s[1] / max(s[0], 1),
@@ -62,6 +62,9 @@ def main():
                             "straddle_buckets_per_pass": s[4] / max(s[1], 1), "team_pairs": s[5],
                             "team_passes_per_pair": s[6] / max(s[5], 1), "team_warp_iterations": s[7],
                             "team_pair_passes": s[6],
+                            "team_by_tau_class": {c: {"warp_iterations": s[12 + i], "pair_passes": s[16 + i],
+                                                      "pairs": s[20 + i]}
+                                                  for i, c in enumerate(["1", "2-4", "8-16", ">=32"])},
                             "bucket_cycles_per_pair": {k: s[8 + i] / max(s[0], 1) for i, k in
                                                        enumerate(["range_sort", "bucket_sums", "passes", "final"])}}
     out["counters"] = g.read_counters(ws, p, args.batch)
@@ -82,6 +85,24 @@ def main():
             mix[k + "_pairs"] += N // L - 1
             mix[k + "_samples"] += (N // L - 1) * L
     out["query_mix"] = mix
+    # team-path queries by team width tau = pow2ceil(ceil(L / 16)) (L < 513): queries, pairs
+    taus = {}
+    for i in range(args.batch):
+        if r[i]["status"] != 0:
+            continue
+        Ls = set(int(v) for v in d[i]["cand_L"][: d[i]["n_candidates"]])
+        Ls |= set(range(int(d[i]["local_lo"]), int(d[i]["local_hi"]) + 1))
+        for L in Ls:
+            if L >= 513:
+                continue
+            tau = 1
+            while tau * 16 < L:
+                tau <<= 1
+            e = taus.setdefault(tau, [0, 0, 0])
+            e[0] += 1
+            e[1] += N // L - 1
+            e[2] += (N // L - 1) * L
+    out["team_taus"] = {str(k): {"queries": v[0], "pairs": v[1], "samples": v[2]} for k, v in sorted(taus.items())}
     hist = np.histogram([int(v) for v in r["period"] if v > 0], bins=[0, 64, 128, 256, 513, 1024, 2048, 4097])
     out["period_hist"] = {"edges": hist[1].tolist(), "counts": hist[0].tolist()}
     print(json.dumps(out))
