@@ -399,19 +399,20 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
             if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
         }
       } else {
+        // the new labels are packed afresh; "any label changed" is one compare of the words
+        uint64_t nl = 0;
 #pragma unroll 1
         for (int u = 0; u < cnt; ++u) {
           const double y = ys[u * kScoreThreads];
           double e[G];
           const int b = cem.assign(y, e);
-          const int sh = 4 * u;
-          const int old = (int)((labs >> sh) & 15u);
-          changed |= (b != old);
-          labs ^= (uint64_t)(old ^ b) << sh;
+          nl |= (uint64_t)b << (4 * u);
 #pragma unroll
           for (int j = 0; j < G; ++j)
             if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
         }
+        changed = nl != labs;
+        labs = nl;
       }
     }
 #if GPOEO_TEAM_RS
