@@ -160,7 +160,9 @@ def test_similarity_scores_match_oracle():
 def test_similarity_groups_and_caps(G, maxit):
     x = tg.generate_host(tg.CFG2, 3, 2)
     ys = np.stack([O.composite(x[b])[0] for b in range(2)])
-    Ls = [7, 20, 64, 300, 600, 1500]
+    # team widths 1, 2, 4, 8, 16, 32 (the halving reduction runs on teams of >= pow2ceil(2G)
+    # lanes, the butterfly on smaller ones) and both bucketed launches
+    Ls = [7, 20, 64, 100, 200, 300, 600, 1500, 3000]
     ti = np.repeat(np.arange(2), len(Ls)).astype(np.int32)
     pe = np.tile(np.array(Ls, np.int32), 2)
     got = g.similarity_error(torch.from_numpy(ys).cuda(), ti, pe, num_groups=G, gmm_max_iters=maxit).cpu().numpy()
