@@ -615,3 +615,31 @@ def test_rolling_and_measure_non_pow2_weighted():
         agree += (int(m[i]["t_iter"]), int(m[i]["rounds"]), int(m[i]["samples"])) == (o["t_iter"], o["rounds"],
                                                                                        o["samples"])
     assert agree >= x.shape[0] - 1
+
+
+def test_sharded_detect_nccl_world1():
+    # row e on the device: shard.detect_sharded through a real NCCL process group (world 1 on
+    # the one GPU a test box has): the all-gathered records equal the unsharded call's bytes
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2201_01684_b200 import shard
+
+    spec = tg.CFG2.with_(batch=12)
+    x = tg.generate_host(spec)
+    p = g.params_for(spec)
+    r1, _, _ = _detect(x, p)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        out, _ = shard.detect_sharded(_to_dev(x), spec.batch, p)
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == r1.tobytes()
+    finally:
+        dist.destroy_process_group()
