@@ -552,6 +552,9 @@ static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* s
   return cudaGetLastError();
 }
 
+#ifndef GPOEO_R2C_PAIR
+#define GPOEO_R2C_PAIR 1
+#endif
 namespace fz {
 constexpr int kN = 65536, kn = 32768, kn2 = 16384, kT = 512;
 constexpr int kBuf = kn2 + kn2 / 32;  // padded float2 entries (>= kn + 1 floats: the full P fits)
@@ -821,6 +824,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     pass<32>(buf, tw, 32);
     pass<16>(buf, tw, 1024);
     // ---- D: R2C post: P[2 k2 + q] (C = 2: partner bins sit in the same CTA) ------------
+    float* P = reinterpret_cast<float*>(buf);
+    const float* Pp = reinterpret_cast<const float*>(pbuf);
+#if GPOEO_R2C_PAIR
+    // bins k and k' = n - k (same parity, so the same CTA) share Z_k, Z_{n-k}: E' = conj(E),
+    // O' = conj(O), W' = -conj(W), hence X' = conj(E - W O): one pair of loads, one twiddle
+    // and one product give both powers |E + W O|^2 and |E - W O|^2. Local index of k' is
+    // m = (kn2 - k2 - q) mod kn2; q = 0, k2 = 0 pairs bin 0 with the Nyquist bin n.
+    constexpr int PPT = kn2 / 2 / kT;  // pairs per thread
+    float pa[PPT], pb[PPT];
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+      const int k2 = threadIdx.x + i * kT;  // < kn2 / 2
+      const int k = 2 * k2 + q;
+      const int m = (kn2 - k2 - q) & (kn2 - 1);
+      const float2 Zk = buf[pad(k2)];
+      const float2 Zp = buf[pad(m)];
+      const float2 E = make_float2(0.5f * (Zk.x + Zp.x), 0.5f * (Zk.y - Zp.y));
+      const float2 O = make_float2(0.5f * (Zk.y + Zp.y), -0.5f * (Zk.x - Zp.x));
+      const float2 W = cmul(twiddle(tw, k >> 2), kW65536[k & 3]);
+      const float2 T = cmul(W, O);
+      const float2 Xa = cadd(E, T), Xb = csub(E, T);
+      pa[i] = Xa.x * Xa.x + Xa.y * Xa.y;
+      pb[i] = Xb.x * Xb.x + Xb.y * Xb.y;
+    }
+    float pmid = 0.f;  // q = 0: bin n/2 (local kn2/2) is its own mirror
+    if (q == 0 && threadIdx.x == 0) {
+      const int k2 = kn2 / 2, k = 2 * k2;
+      const float2 Zk = buf[pad(k2)];
+      const float2 E = make_float2(Zk.x, 0.f);
+      const float2 O = make_float2(Zk.y, 0.f);
+      const float2 W = cmul(twiddle(tw, k >> 2), kW65536[k & 3]);
+      const float2 X = cadd(E, cmul(W, O));
+      pmid = X.x * X.x + X.y * X.y;
+    }
+    __syncthreads();  // my Z fully read (C = 2: the R2C partner bins are local)
+    // my bins in place: P_loc[k2] = P[2 k2 + q]; the neighbours of my bins are the
+    // partner's (DSMEM reads in phase E)
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+      const int k2 = threadIdx.x + i * kT;
+      const int m = (kn2 - k2 - q) & (kn2 - 1);
+      const int mi = (q == 0 && k2 == 0) ? kn2 : m;  // q = 0, k2 = 0: the mirror is bin n
+      P[k2] = pa[i];
+      P[mi] = pb[i];
+      if (spectra) {
+        spectra[t * (int64_t)(kn + 1) + 2 * k2 + q] = pa[i];
+        spectra[t * (int64_t)(kn + 1) + 2 * mi + q] = pb[i];
+      }
+    }
+    if (q == 0 && threadIdx.x == 0) {
+      P[kn2 / 2] = pmid;
+      if (spectra) spectra[t * (int64_t)(kn + 1) + kn2] = pmid;
+    }
+#else
     constexpr int PER = kn2 / kT;
     float pv[PER];
 #pragma unroll
@@ -845,8 +902,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     __syncthreads();  // my Z fully read (C = 2: the R2C partner bins are local)
     // my bins in place: P_loc[k2] = P[2 k2 + q]; the neighbours of my bins are the
     // partner's (DSMEM reads in phase E)
-    float* P = reinterpret_cast<float*>(buf);
-    const float* Pp = reinterpret_cast<const float*>(pbuf);
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
       const int k2 = threadIdx.x + i * kT;
@@ -857,6 +912,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       P[kn2] = pnyq;
       if (spectra) spectra[t * (int64_t)(kn + 1) + kn] = pnyq;
     }
+#endif
     if (mode == kPeaksCandidates && q == 0 && threadIdx.x == 0) fs.ps.count = 0;
     cluster.sync();
     // ---- E: peaks over my bins k = 2 k2 + q of the band ----------------------------------
