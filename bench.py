@@ -312,7 +312,7 @@ def run_gpu(args) -> None:
         mgbs = mbytes / (mms / 1e3) / 1e9
         line["spectral_only"] = {
             "metric": "traces/sec spectral-only period (T_iter = 1/f_major, P:291)", "value": world * B / (mms / 1e3),
-            "unit": "traces/s", "ms_per_step": mms, "kernel": "fused_spectrum_65536<3> (mode major), 1 launch/step",
+            "unit": "traces/s", "ms_per_step": mms, "kernel": "fused_spectrum_65536<3> (mode major) + major_combine_kernel, 2 launches/step",
             "roofline": {"bound": "hbm", "achieved": mgbs, "peak": hbm_peak, "unit": "GB/s", "frac": mgbs / hbm_peak,
                          "traffic": traffic_spec, "peak_kind": peak_kind,
                          "bytes": f"{4 * spec.n_features * spec.n_samples + g.MAJOR_DTYPE.itemsize} B/trace"}}

@@ -552,6 +552,9 @@ static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* s
   return cudaGetLastError();
 }
 
+#ifndef GPOEO_MAJOR_SPLIT
+#define GPOEO_MAJOR_SPLIT 1
+#endif
 #ifndef GPOEO_R2C_PAIR
 #define GPOEO_R2C_PAIR 1
 #endif
@@ -947,11 +950,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
           const int32_t ok = fs.ps.redk[i];
           if (op > bp || (op == bp && ok < bk)) { bp = op; bk = ok; }
         }
+#if GPOEO_MAJOR_SPLIT
+        if (mode == kPeaksMajor) {
+          // no cluster barrier: each rank leaves its (P, k) best in its half of the 16-B
+          // result record (P = -2 marks a constant trace); major_combine_kernel finishes it
+          reinterpret_cast<int2*>(&w.major[t])[q] =
+              make_int2(__float_as_int(all_const ? -2.f : bp), bk);
+        }
+#endif
         fs.pm[q] = bp;
         fs.pk[q] = bk;
         pfs->pm[q] = bp;
         pfs->pk[q] = bk;
       }
+#if GPOEO_MAJOR_SPLIT
+      if (mode == kPeaksMajor) continue;  // the next trace's first barrier orders buffer reuse
+#endif
       cluster.sync();
       float pmax = fs.pm[0];
       int32_t kmax = fs.pk[0];
@@ -1022,16 +1036,47 @@ static cudaError_t launch_fused_65536(const Plan& p, const float* x, Work w, flo
   return cudaGetLastError();
 }
 
+// Spectral-only mode of the fused kernel: combine the two ranks' in-band maxima left in
+// each result record ((P_0, k_0), (P_1, k_1); P_0 = -2 for a constant trace) into the
+// record, with exactly the status / tie rules of the barrier version (largest P, then
+// smallest k; R3)
+__global__ void major_combine_kernel(Plan p, gpoeo_major_result* r) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= p.batch) return;
+  const int4 v = *reinterpret_cast<const int4*>(&r[t]);
+  const float pm0 = __int_as_float(v.x), pm1 = __int_as_float(v.z);
+  float pmax = pm0;
+  int32_t kmax = v.y;
+  if (pm1 > pmax || (pm1 == pmax && v.w < kmax)) { pmax = pm1; kmax = v.w; }
+  int32_t status = pm0 == -2.f ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
+  if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;
+  if (status == GPOEO_TRACE_OK && pmax < 0.f) status = GPOEO_TRACE_APERIODIC;
+  gpoeo_major_result o;
+  o.status = status;
+  o.bin = status == GPOEO_TRACE_OK ? kmax : -1;
+  o.period = status == GPOEO_TRACE_OK ? p.N / kmax : -1;
+  o.period_s = status == GPOEO_TRACE_OK ? (float)((double)o.period * p.Ts) : -1.f;
+  r[t] = o;
+}
+
 cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
                                   int mode, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
   if (p.N != fz::kN) return cudaErrorInvalidValue;
+  cudaError_t e;
   switch (p.F) {
-    case 1: return launch_fused_65536<1>(p, x, w, y_out, spectra, mode, s);
-    case 2: return launch_fused_65536<2>(p, x, w, y_out, spectra, mode, s);
-    case 3: return launch_fused_65536<3>(p, x, w, y_out, spectra, mode, s);
+    case 1: e = launch_fused_65536<1>(p, x, w, y_out, spectra, mode, s); break;
+    case 2: e = launch_fused_65536<2>(p, x, w, y_out, spectra, mode, s); break;
+    case 3: e = launch_fused_65536<3>(p, x, w, y_out, spectra, mode, s); break;
     default: return cudaErrorInvalidValue;
   }
+#if GPOEO_MAJOR_SPLIT
+  if (e == cudaSuccess && mode == kPeaksMajor) {
+    major_combine_kernel<<<(unsigned)((p.batch + 255) / 256), 256, 0, s>>>(p, w.major);
+    e = cudaGetLastError();
+  }
+#endif
+  return e;
 }
 
 
