@@ -144,9 +144,9 @@ int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_p
  *  host_traces  HOST [batch][trace_stride] fp32 (pinned memory gives async overlap);
  *  host_results HOST [batch] gpoeo_result.
  * Streams chunks of at most `chunk` traces through the workspace (size it with
- * gpoeo_workspace_size_host: three chunk buffers in flight; the first two chunks hold chunk/4
+ * gpoeo_workspace_size_host: four chunk buffers in flight; the first two chunks hold chunk/4
  * and chunk/2 traces so compute starts early), overlapping H2D copies with
- * compute on an internal copy stream and two compute streams; result copies are issued three
+ * compute on an internal copy stream and three compute streams; result copies are issued four
  * chunks late so a pageable host_results never stalls the pipeline. SYNCHRONISES `stream`
  * before returning (results are on the host). */
 size_t gpoeo_workspace_size_host(const gpoeo_params* p, int64_t chunk);
