@@ -539,7 +539,7 @@ int gpoeo_detect_periods_host(const float* host_traces, int64_t batch, const gpo
   }
   cfirst.push_back(batch);
   const int64_t nchunks = (int64_t)cfirst.size() - 1;
-  // results of chunk c leave through the copy stream when buffer c % 3 is reused (or at the
+  // results of chunk c leave through the copy stream when buffer c % kHostBuffers is reused (or at the
   // end): a D2H copy into pageable host memory blocks the host until it completes, so it is
   // issued kHostBuffers chunks late, while the chunks after it keep the GPU busy
   auto drain = [&](int64_t c) -> int {
