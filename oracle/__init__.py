@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
@@ -25,6 +26,12 @@ _SRC = os.path.join(_HERE, "gpoeo_oracle.c")
 _SO = os.path.join(_HERE, "liboracle.so")
 
 TRACE_OK, TRACE_APERIODIC, TRACE_INSUFFICIENT, TRACE_CONSTANT, TRACE_UNSTABLE = 0, 1, 2, 3, 4
+
+# Z27 thresholds (the same numbers as oracle_ambiguous() in gpoeo_oracle.c): a
+# decision margin below these has several correct outcomes -- spectral decisions relative to
+# P_max (fp32 FFT vs fp64 DFT), Err comparisons relative (reordered fp64 sums), CEM decisions
+# relative to the score magnitude
+THR_SPEC, THR_ERR, THR_CEM = 1e-5, 1e-9, 1e-10
 
 
 class OrParams(ctypes.Structure):
@@ -70,6 +77,8 @@ class OrResult(ctypes.Structure):
         ("n_queries", ctypes.c_int64),
         ("samples_clustered", ctypes.c_int64),
         ("cem_sample_iters", ctypes.c_int64),
+        ("d_order", ctypes.c_double),
+        ("cand_margin", ctypes.c_double * 32),
     ]
 
 
@@ -81,7 +90,7 @@ class OrMajor(ctypes.Structure):
 
 class OrRolling(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("t_init", ctypes.c_int32), ("t_iter", ctypes.c_int32),
-                ("n_sub", ctypes.c_int32), ("early", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("n_sub", ctypes.c_int32), ("early", ctypes.c_int32), ("amb", ctypes.c_int32),
                 ("err_init", ctypes.c_double), ("err_iter", ctypes.c_double), ("diff", ctypes.c_double),
                 ("smpdur_next", ctypes.c_double), ("sub_start", ctypes.c_int32 * 64),
                 ("sub_period", ctypes.c_int32 * 64), ("sub_err", ctypes.c_double * 64)]
@@ -90,7 +99,7 @@ class OrRolling(ctypes.Structure):
 class OrMeasure(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("t_iter", ctypes.c_int32), ("rounds", ctypes.c_int32),
                 ("samples", ctypes.c_int32), ("measure_start", ctypes.c_int32), ("measure_end", ctypes.c_int32),
-                ("err_iter", ctypes.c_double)]
+                ("amb", ctypes.c_int32), ("pad", ctypes.c_int32), ("err_iter", ctypes.c_double)]
 
 
 class OrGearWorkload(ctypes.Structure):
@@ -100,20 +109,32 @@ class OrGearWorkload(ctypes.Structure):
 
 class OrGearResult(ctypes.Structure):
     _fields_ = [("sm_gear", ctypes.c_int32), ("mem_gear", ctypes.c_int32), ("probes_sm", ctypes.c_int32),
-                ("probes_mem", ctypes.c_int32), ("objective", ctypes.c_double)]
+                ("probes_mem", ctypes.c_int32), ("objective", ctypes.c_double), ("margin_rel", ctypes.c_double),
+                ("margin_round", ctypes.c_double)]
 
 
 def build() -> str:
     """Compile the oracle (gcc, fp64, no FMA contraction). Building the checker is not using it."""
     if not (os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC)):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
+        tmp = f"{_SO}.{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _SO)  # atomic: a concurrent loader never sees a partial file
     return _SO
 
 
 _lib = None
+_lock = threading.Lock()
 
 
 def _L():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        return _load_locked()
+
+
+def _load_locked():
     global _lib
     if _lib is None:
         lib = ctypes.CDLL(build())
@@ -136,6 +157,11 @@ def _L():
         lib.oracle_local_range.restype = None
         lib.oracle_detect.argtypes = [P, ctypes.POINTER(OrParams), P, ctypes.POINTER(OrResult), P]
         lib.oracle_detect.restype = ctypes.c_int
+        lib.oracle_detect_ex.argtypes = [P, ctypes.POINTER(OrParams), P, ctypes.c_int32, P, ctypes.c_int32,
+                                         ctypes.POINTER(OrResult), P, P]
+        lib.oracle_detect_ex.restype = ctypes.c_int
+        lib.oracle_ambiguous.argtypes = [ctypes.POINTER(OrResult)]
+        lib.oracle_ambiguous.restype = ctypes.c_int
         lib.oracle_exhaustive.argtypes = [P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, P]
         lib.oracle_exhaustive.restype = ctypes.c_int32
@@ -287,31 +313,47 @@ class Detection:
     local_hi: int
     local_err: np.ndarray
     margins: dict = field(default_factory=dict)
+    cand_margin: list = field(default_factory=list)
+    local_margin: np.ndarray | None = None
     counters: dict = field(default_factory=dict)
     n_peaks: int = 0
     n_passing: int = 0
     cap_binds: bool = False
 
-    def ambiguous(self, thr_spec=1e-4, thr_err=1e-9, thr_cem=1e-10) -> bool:
+    def ambiguous(self, thr_spec=THR_SPEC, thr_err=THR_ERR, thr_cem=THR_CEM) -> bool:
         """Z27: several results are correct when a decision's margin is below what the
         precision difference between the two sides can move (fp32 spectrum vs fp64 DFT;
         reordered fp64 sums)."""
+        return bool(self.amb_reasons(thr_spec, thr_err, thr_cem))
+
+    def amb_reasons(self, thr_spec=THR_SPEC, thr_err=THR_ERR, thr_cem=THR_CEM) -> list:
+        """The Z27 margins below their thresholds (spectral: of P_max; err: relative; cem:
+        relative CEM score gap), by name."""
         m = self.margins
-        return (m["d_thr"] < thr_spec or m["d_peak"] < thr_spec or m["d_rank"] < thr_spec
-                or m["d_err_cand"] < thr_err or m["d_err_local"] < thr_err or m["d_cem"] < thr_cem)
+        th = dict(d_thr=thr_spec, d_peak=thr_spec, d_rank=thr_spec, d_order=thr_spec, d_err_cand=thr_err,
+                  d_err_local=thr_err, d_cem=thr_cem)
+        return [k for k, t in th.items() if m[k] < t]
 
 
-def detect(x: np.ndarray, params: Params) -> Detection:
-    """Alg. 1 on one trace x float32 [F][N]."""
+def detect(x: np.ndarray, params: Params, given_k=None, force_kb: int = -1) -> Detection:
+    """Alg. 1 on one trace x float32 [F][N].
+
+    Test hooks of the parity harness (oracle_detect_ex): given_k = a candidate bin list to use
+    instead of O2-O3 (Alg. 1 from line 6 on another side's candidates); force_kb = the bin to
+    take as Tcand_opt instead of the argmin."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     p = params.c()
     r = OrResult()
     le = np.full(max(1, p.max_period - p.min_period + 1), np.nan)
+    lm = np.full(le.size, np.nan)
     # the ABI carries w_c as fp32: use the same values
     w = None if params.weights is None else np.asarray(params.weights, np.float32).astype(np.float64)
-    rc = _L().oracle_detect(_ptr(x), ctypes.byref(p), None if w is None else _ptr(w), ctypes.byref(r), _ptr(le))
+    gk = None if given_k is None else np.ascontiguousarray(given_k, np.int32)
+    rc = _L().oracle_detect_ex(_ptr(x), ctypes.byref(p), None if w is None else _ptr(w),
+                               -1 if gk is None else gk.size, None if gk is None else _ptr(gk), int(force_kb),
+                               ctypes.byref(r), _ptr(le), _ptr(lm))
     if rc != 0:
-        raise ValueError("oracle_detect: invalid parameters")
+        raise ValueError(f"oracle_detect_ex: rc {rc}")
     nc = r.n_candidates
     nloc = (r.local_hi - r.local_lo + 1) if r.status == TRACE_OK else 0
     return Detection(
@@ -319,8 +361,9 @@ def detect(x: np.ndarray, params: Params) -> Detection:
         best_candidate=r.best_candidate, best_bin=r.best_bin, n_candidates=nc,
         cand_k=list(r.cand_k[:nc]), cand_L=list(r.cand_L[:nc]), cand_err=list(r.cand_err[:nc]),
         cand_P=list(r.cand_P[:nc]), local_lo=r.local_lo, local_hi=r.local_hi, local_err=le[:nloc].copy(),
-        margins=dict(d_thr=r.d_thr, d_peak=r.d_peak, d_rank=r.d_rank, d_err_cand=r.d_err_cand,
+        margins=dict(d_thr=r.d_thr, d_peak=r.d_peak, d_rank=r.d_rank, d_order=r.d_order, d_err_cand=r.d_err_cand,
                      d_err_local=r.d_err_local, d_cem=r.d_cem),
+        cand_margin=list(r.cand_margin[:nc]), local_margin=lm[:nloc].copy(),
         counters=dict(n_queries=r.n_queries, samples_clustered=r.samples_clustered,
                       cem_sample_iters=r.cem_sample_iters),
         n_peaks=r.n_peaks, n_passing=r.n_passing, cap_binds=bool(r.cap_binds))
@@ -353,7 +396,7 @@ class Major:
     d_major: float
     d_peak: float
 
-    def ambiguous(self, thr_spec=1e-4) -> bool:
+    def ambiguous(self, thr_spec=THR_SPEC) -> bool:
         """Z27: the fp32 FFT may order two peaks within thr_spec of P_major either way."""
         return self.d_major < thr_spec or self.d_peak < thr_spec
 
@@ -388,6 +431,7 @@ class Rolling:
     sub_start: list
     sub_period: list
     sub_err: list
+    amb: bool = False  # Z27: some decision of the call had several correct outcomes
 
 
 def rolling(x: np.ndarray, params: Params, c_measure: float = 2.0, step: float = 0.5, c_eval: float = 6.5,
@@ -402,7 +446,7 @@ def rolling(x: np.ndarray, params: Params, c_measure: float = 2.0, step: float =
     n = r.n_sub
     return Rolling(status=r.status, t_init=r.t_init, t_iter=r.t_iter, early=bool(r.early), diff=r.diff,
                    smpdur_next=r.smpdur_next, sub_start=list(r.sub_start[:n]), sub_period=list(r.sub_period[:n]),
-                   sub_err=list(r.sub_err[:n]))
+                   sub_err=list(r.sub_err[:n]), amb=bool(r.amb))
 
 
 def measure(x: np.ndarray, params: Params, init: int, c_measure: float = 2.0, step: float = 0.5,
@@ -416,7 +460,7 @@ def measure(x: np.ndarray, params: Params, init: int, c_measure: float = 2.0, st
                            diff_threshold, ctypes.byref(m)) != 0:
         raise ValueError("oracle_measure: invalid parameters")
     return dict(status=m.status, t_iter=m.t_iter, rounds=m.rounds, samples=m.samples,
-                measure_start=m.measure_start, measure_end=m.measure_end, err_iter=m.err_iter)
+                measure_start=m.measure_start, measure_end=m.measure_end, err_iter=m.err_iter, amb=bool(m.amb))
 
 
 def gear_workload(**kw) -> OrGearWorkload:
@@ -441,4 +485,4 @@ def gear_search(w: OrGearWorkload, sm_mhz, mem_mhz, cap: float, pred_sm: int, pr
                                ctypes.byref(r)) != 0:
         raise ValueError("oracle_gear_search: invalid arguments")
     return dict(sm_gear=r.sm_gear, mem_gear=r.mem_gear, probes_sm=r.probes_sm, probes_mem=r.probes_mem,
-                objective=r.objective)
+                objective=r.objective, margin_rel=r.margin_rel, margin_round=r.margin_round)

@@ -7,16 +7,16 @@
  * (paper_2201_01684_b200/) never links, imports or calls it, and shares no code,
  * header, table or constant generator with it.
  *
- * Everything is fp64 on the fp32 input bytes (except the composite signal itself, formed
- * in fp32 from fp64 statistics: reading Z23b), sequential loops in the order the paper
- * writes them, one trace per call (callers parallelise over traces).
+ * Everything is fp64 on the fp32 input bytes (the composite signal is the fp64 expression
+ * rounded to fp32 once: reading Z23), sequential loops in the order the paper writes them,
+ * one trace per call (callers parallelise over traces).
  * Compiled with -O2 -ffp-contract=off (no FMA contraction).
  *
  * Citations: P:n = /root/reference/PAPER.md line n. Readings Z1..Z30 are the ones
  * listed in SURVEY.md 8(c) and DESIGN.md "Readings".
  *
  * Steps:
- *   O1 composite detection signal              P:459 (+ Z1, Z23b)
+ *   O1 composite detection signal              P:459 (+ Z1, Z23)
  *   O2 power spectrum by the DFT definition     Alg.1 l.1-2, P:309-310 (+ Z2-Z4)
  *   O3 peaks -> candidate integer periods       Alg.1 l.3-5, P:311-314 (+ Z5-Z9, Z21)
  *   O4 Alg. 2 similarity error per candidate    P:353-382 (+ Z10-Z16)
@@ -87,22 +87,26 @@ typedef struct {
   int64_t n_queries;
   int64_t samples_clustered; /* sum over queries of (M-1)*L               */
   int64_t cem_sample_iters;  /* sum over windows of passes*L              */
+  /* Z27 margins added for the parity harness: d_order = min |P_i - P_{i+1}| / P_max over
+   * consecutive ranked peaks among the first min(passing, K+1) (ties in the rank order,
+   * the dedupe and the K cap); cand_margin[q] = the CEM decision margin of candidate q's
+   * Alg. 2 evaluation (min over its windows) */
+  double d_order;
+  double cand_margin[32];
 } or_result;
 
 /* ------------------------------------------------------------------------ */
 /* O1. Composite detection signal (P:459 names a composite of power, SM util and
  * mem util; Z1 reading: population z-score per channel, weighted sum, sigma=0
- * channel contributes 0). Statistics in fp64 (two passes, Z23):
- *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N);
- * the centre and scale are rounded to fp32 once per channel (reading Z23b),
- *   m_c = fp32(mu_c),  s_c = fp32(w_c / sigma_c),
- * and the signal is formed in fp32, channel order, each operation rounded to nearest
- * (no FMA):  y[n] = (...((0 + s_0 (x_0[n] - m_0)) + s_1 (x_1[n] - m_1)) + ...).
+ * channel contributes 0; Z23 reading: the expression is evaluated in fp64 and y is
+ * rounded to fp32 once):
+ *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N),
+ *   y[n] = fp32( sum_c a_c (x_c[n] - mu_c) ),  a_c = w_c / sigma_c
+ * (the scale a_c is formed once per channel, products and sums in channel order, no FMA).
  * Returns 1 if every channel is constant. mu/sigma may be NULL. */
 int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, float* y, double* mu_out,
                      double* sigma_out) {
-  double mu[8], sigma[8];
-  float m[8], sc[8];
+  double mu[8], sigma[8], a[8];
   int all_const = 1;
   for (int c = 0; c < F; ++c) {
     const float* xc = x + (int64_t)c * N;
@@ -112,22 +116,17 @@ int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, floa
     double q = 0.0;
     for (int n = 0; n < N; ++n) q += ((double)xc[n] - mu[c]) * ((double)xc[n] - mu[c]);
     sigma[c] = sqrt(q / N);
-    m[c] = (float)mu[c];
-    sc[c] = sigma[c] > 0.0 ? (float)((w ? w[c] : 1.0) / sigma[c]) : 0.0f;
+    a[c] = sigma[c] > 0.0 ? (w ? w[c] : 1.0) / sigma[c] : 0.0;
     if (sigma[c] > 0.0) all_const = 0;
     if (mu_out) mu_out[c] = mu[c];
     if (sigma_out) sigma_out[c] = sigma[c];
   }
   for (int n = 0; n < N; ++n) {
-    float v = 0.0f;
+    double v = 0.0;
     for (int c = 0; c < F; ++c) {
-      if (sigma[c] > 0.0) {
-        const float d = x[(int64_t)c * N + n] - m[c];
-        const float t = sc[c] * d;
-        v = v + t;
-      }
+      if (sigma[c] > 0.0) v += a[c] * ((double)x[(int64_t)c * N + n] - mu[c]);
     }
-    y[n] = v;
+    y[n] = (float)v;
   }
   return all_const;
 }
@@ -383,6 +382,14 @@ int oracle_candidates(const double* P, const or_params* p, or_result* r) {
     if (m2 < r->d_peak) r->d_peak = m2;
   }
   if (passing > K) r->d_rank = fabs(P[pk[K - 1]] - P[pk[K]]) / pmax;
+  r->d_order = INFINITY;
+  {
+    const int lim = passing < K + 1 ? passing : K + 1;
+    for (int i = 0; i + 1 < lim; ++i) {
+      double m = fabs(P[pk[i]] - P[pk[i + 1]]) / pmax;
+      if (m < r->d_order) r->d_order = m;
+    }
+  }
   /* top-K, threshold, integer period, dedupe */
   int nc = 0;
   for (int i = 0; i < npk && i < K; ++i) {
@@ -424,18 +431,28 @@ static double rel_gap(double best, double second) {
 
 /* ------------------------------------------------------------------------ */
 /* Alg. 1 on one trace x[F][N]. local_err (optional) receives Err for each L in
- * [local_lo, local_hi]; size >= L_max - L_min + 1. */
-int oracle_detect(const float* x, const or_params* p, const double* weights, or_result* r, double* local_err) {
+ * [local_lo, local_hi]; size >= L_max - L_min + 1; local_margin (optional, same size) the
+ * CEM decision margin of each of those Alg. 2 evaluations.
+ * Test hooks (the parity harness's validity checks, never used with the defaults):
+ *  n_given >= 0: skip O2-O3 and take the n_given candidate bins given_k[] (L = floor(N/k),
+ *                in that order) -- Alg. 1 from line 6 on another side's candidate list;
+ *  force_kb >= 0: take the candidate of bin force_kb as Tcand_opt (line 10) instead of the
+ *                argmin (it must be one of the candidates; else -2). */
+int oracle_detect_ex(const float* x, const or_params* p, const double* weights, int32_t n_given,
+                     const int32_t* given_k, int32_t force_kb, or_result* r, double* local_err,
+                     double* local_margin) {
   memset(r, 0, sizeof(*r));
   const int32_t N = p->n_samples;
   if (N < 8 || p->n_features < 1 || p->n_features > 8 || p->min_period < 2 || p->max_period < p->min_period ||
       p->max_period > N / 2 || p->max_candidates < 1 || p->max_candidates > 32 || p->num_groups < 1 ||
-      p->num_groups > 8 || p->gmm_max_iters < 1 || !(p->c_peak > 0.0) || p->c_peak > 1.0)
+      p->num_groups > 8 || p->gmm_max_iters < 1 || !(p->c_peak > 0.0) || p->c_peak > 1.0 || n_given > 32)
     return -1;
+  int rc = 0;
   r->period = -1;
   r->best_candidate = -1;
   r->best_bin = -1;
-  r->d_thr = r->d_peak = r->d_rank = r->d_err_cand = r->d_err_local = r->d_cem = INFINITY;
+  r->d_thr = r->d_peak = r->d_rank = r->d_order = r->d_err_cand = r->d_err_local = r->d_cem = INFINITY;
+  for (int q = 0; q < 32; ++q) r->cand_margin[q] = INFINITY;
   float* y = (float*)malloc(sizeof(float) * N);
   double* P = (double*)malloc(sizeof(double) * (N / 2 + 1));
   /* O1 */
@@ -447,30 +464,43 @@ int oracle_detect(const float* x, const or_params* p, const double* weights, or_
     for (int64_t k = 1; k <= N / 2; ++k) any |= in_band(N, k, p->min_period, p->max_period);
     if (!any || N < 2 * p->min_period) { r->status = OR_TRACE_INSUFFICIENT; goto done; }
   }
-  /* O2 */
-  if (p->dft_band_only) {
-    int32_t k0 = N, k1 = 0;
-    for (int64_t k = 1; k <= N / 2; ++k)
-      if (in_band(N, k, p->min_period, p->max_period)) {
-        if (k < k0) k0 = (int32_t)k;
-        if (k > k1) k1 = (int32_t)k;
-      }
-    for (int k = 0; k <= N / 2; ++k) P[k] = NAN;
-    k0 = k0 - 1 < 0 ? 0 : k0 - 1;
-    k1 = k1 + 1 > N / 2 ? N / 2 : k1 + 1;
-    oracle_power_spectrum_range(y, N, k0, k1, P);
-    if (k1 == N / 2 && N / 2 - 1 < k0) oracle_power_spectrum_range(y, N, N / 2 - 1, N / 2 - 1, P);
+  if (n_given >= 0) {
+    /* test hook: the candidate list of another side */
+    for (int q = 0; q < n_given; ++q) {
+      r->cand_k[q] = given_k[q];
+      r->cand_L[q] = N / given_k[q];
+      r->cand_P[q] = NAN;
+    }
+    r->n_candidates = n_given;
+    if (n_given == 0) { r->status = OR_TRACE_APERIODIC; goto done; }
   } else {
-    oracle_power_spectrum(y, N, P);
+    /* O2 */
+    if (p->dft_band_only) {
+      int32_t k0 = N, k1 = 0;
+      for (int64_t k = 1; k <= N / 2; ++k)
+        if (in_band(N, k, p->min_period, p->max_period)) {
+          if (k < k0) k0 = (int32_t)k;
+          if (k > k1) k1 = (int32_t)k;
+        }
+      for (int k = 0; k <= N / 2; ++k) P[k] = NAN;
+      k0 = k0 - 1 < 0 ? 0 : k0 - 1;
+      k1 = k1 + 1 > N / 2 ? N / 2 : k1 + 1;
+      oracle_power_spectrum_range(y, N, k0, k1, P);
+      if (k1 == N / 2 && N / 2 - 1 < k0) oracle_power_spectrum_range(y, N, N / 2 - 1, N / 2 - 1, P);
+    } else {
+      oracle_power_spectrum(y, N, P);
+    }
+    /* O3 */
+    if (oracle_candidates(P, p, r) == 0) { r->status = OR_TRACE_APERIODIC; goto done; }
   }
-  /* O3 */
-  if (oracle_candidates(P, p, r) == 0) { r->status = OR_TRACE_APERIODIC; goto done; }
   /* O4 + O5 */
   int best = -1;
   for (int q = 0; q < r->n_candidates; ++q) {
-    double e = oracle_similarity_error(y, N, r->cand_L[q], p->num_groups, p->gmm_max_iters, &r->d_cem,
-                                       &r->cem_sample_iters);
+    double m = INFINITY;
+    double e = oracle_similarity_error(y, N, r->cand_L[q], p->num_groups, p->gmm_max_iters, &m, &r->cem_sample_iters);
     r->cand_err[q] = e;
+    r->cand_margin[q] = m;
+    if (m < r->d_cem) r->d_cem = m;
     r->n_queries++;
     r->samples_clustered += (int64_t)(N / r->cand_L[q] - 1) * r->cand_L[q];
     if (best < 0 || e < r->cand_err[best] || (e == r->cand_err[best] && r->cand_L[q] < r->cand_L[best])) best = q;
@@ -480,6 +510,13 @@ int oracle_detect(const float* x, const or_params* p, const double* weights, or_
     for (int q = 0; q < r->n_candidates; ++q)
       if (q != best && r->cand_err[q] < second) second = r->cand_err[q];
     r->d_err_cand = rel_gap(r->cand_err[best], second);
+  }
+  if (force_kb >= 0) {
+    int f = -1;
+    for (int q = 0; q < r->n_candidates; ++q)
+      if (r->cand_k[q] == force_kb) f = q;
+    if (f < 0) { rc = -2; goto done; }
+    best = f;
   }
   r->best_candidate = r->cand_L[best];
   r->best_bin = r->cand_k[best];
@@ -491,15 +528,17 @@ int oracle_detect(const float* x, const or_params* p, const double* weights, or_
   /* O7 */
   double* le = local_err ? local_err : (double*)malloc(sizeof(double) * (hi - lo + 1));
   for (int32_t L = lo; L <= hi; ++L) {
-    double e = -1.0;
+    double e = -1.0, m = INFINITY;
     for (int q = 0; q < r->n_candidates; ++q)
-      if (r->cand_L[q] == L) e = r->cand_err[q]; /* memoised: the same Alg.2 value */
+      if (r->cand_L[q] == L) { e = r->cand_err[q]; m = r->cand_margin[q]; } /* memoised: the same Alg.2 value */
     if (e < 0.0) {
-      e = oracle_similarity_error(y, N, L, p->num_groups, p->gmm_max_iters, &r->d_cem, &r->cem_sample_iters);
+      e = oracle_similarity_error(y, N, L, p->num_groups, p->gmm_max_iters, &m, &r->cem_sample_iters);
+      if (m < r->d_cem) r->d_cem = m;
       r->n_queries++;
       r->samples_clustered += (int64_t)(N / L - 1) * L;
     }
     le[L - lo] = e;
+    if (local_margin) local_margin[L - lo] = m;
   }
   int32_t Lbest = lo;
   for (int32_t L = lo + 1; L <= hi; ++L)
@@ -516,7 +555,19 @@ int oracle_detect(const float* x, const or_params* p, const double* weights, or_
 done:
   free(y);
   free(P);
-  return 0;
+  return rc;
+}
+
+int oracle_detect(const float* x, const or_params* p, const double* weights, or_result* r, double* local_err) {
+  return oracle_detect_ex(x, p, weights, -1, NULL, -1, r, local_err, NULL);
+}
+
+/* Z27: a decision of Alg. 1 whose margin is below what the precision difference
+ * between two correct implementations can move (fp32 FFT vs the fp64 DFT: 1e-5 of P_max;
+ * reordered fp64 sums: 1e-9 of Err, 1e-10 of a CEM score) has several correct outcomes. */
+int oracle_ambiguous(const or_result* r) {
+  return r->d_thr < 1e-5 || r->d_peak < 1e-5 || r->d_rank < 1e-5 || r->d_order < 1e-5 || r->d_err_cand < 1e-9 ||
+         r->d_err_local < 1e-9 || r->d_cem < 1e-10;
 }
 
 /* ------------------------------------------------------------------------ */
@@ -628,7 +679,10 @@ typedef struct {
   int32_t t_iter;           /* T_iter (samples)                                          */
   int32_t n_sub;            /* suffixes evaluated                                        */
   int32_t early;            /* 1: lines 3-6 ended the call                               */
-  int32_t pad;
+  int32_t amb;              /* Z27: a decision of the call had several correct outcomes: an
+                               ambiguous Alg. 1 (oracle_ambiguous) on the whole trace or a
+                               suffix, suffix errors of different periods within 1e-9
+                               (line 14), or Diff within 1e-9 of Diff_threshold (line 17)  */
   double err_init;
   double err_iter;
   double diff;
@@ -644,6 +698,7 @@ int oracle_rolling(const float* x, const or_params* p, const double* weights, do
   const int32_t N = p->n_samples;
   or_result r;
   if (oracle_detect(x, p, weights, &r, NULL) != 0) return -1;
+  out->amb = r.status == OR_TRACE_OK && oracle_ambiguous(&r);
   out->status = r.status;
   out->t_init = r.period;
   out->err_init = r.error;
@@ -675,9 +730,12 @@ int oracle_rolling(const float* x, const or_params* p, const double* weights, do
     out->sub_start[n] = s0;
     out->sub_period[n] = -1;
     out->sub_err[n] = 0.0;
-    if (q.min_period <= q.max_period && oracle_detect(y + s0, &q, NULL, &rj, NULL) == 0 && rj.status == OR_TRACE_OK) {
-      out->sub_period[n] = rj.period;
-      out->sub_err[n] = rj.error;
+    if (q.min_period <= q.max_period && oracle_detect(y + s0, &q, NULL, &rj, NULL) == 0) {
+      if (rj.status == OR_TRACE_OK) {
+        out->sub_period[n] = rj.period;
+        out->sub_err[n] = rj.error;
+        if (oracle_ambiguous(&rj)) out->amb = 1;
+      }
     }
     ++n;
     t_start += step * L0;
@@ -707,6 +765,11 @@ int oracle_rolling(const float* x, const or_params* p, const double* weights, do
     out->err_iter = out->sub_err[k];
     out->diff = fabs((tmax - tmin) / (tsum / cnt));
     out->smpdur_next = out->diff < diff_threshold ? -1.0 : ceil(smpdur / tmax) * tmax - smpdur;
+    for (int j = 0; j < n; ++j) /* line 14 near-ties between different periods */
+      if (out->sub_period[j] >= 0 && out->sub_period[j] != out->t_iter &&
+          rel_gap(out->sub_err[k], out->sub_err[j]) < 1e-9)
+        out->amb = 1;
+    if (fabs(out->diff - diff_threshold) < 1e-9 * (diff_threshold > 1.0 ? diff_threshold : 1.0)) out->amb = 1;
   }
   free(y);
   return 0;
@@ -729,6 +792,8 @@ typedef struct {
   int32_t samples;
   int32_t measure_start;
   int32_t measure_end;
+  int32_t amb;   /* Z27: some round's Alg. 3 call was ambiguous (or_rolling.amb) */
+  int32_t pad;
   double err_iter;
 } or_measure;
 
@@ -761,6 +826,7 @@ int oracle_measure(const float* x, const or_params* p, const double* weights, in
     out->status = r.status;
     out->t_iter = r.t_iter;
     out->err_iter = r.err_iter;
+    if (r.amb) out->amb = 1;
     if (r.status == OR_TRACE_OK && r.smpdur_next > 0.0) {
       if ((double)n + r.smpdur_next > (double)Nmax) {
         out->status = OR_TRACE_UNSTABLE;
@@ -805,6 +871,12 @@ typedef struct {
 typedef struct {
   int32_t sm_gear, mem_gear, probes_sm, probes_mem;
   double objective;
+  /* Z27 margins of the search's decisions (the parity harness's validity check): margin_rel =
+   * min relative gap |a - b| / max(|a|, |b|) over every comparison of two objective values
+   * (bracket, golden section, best probe) and the relative cancellation |dA| / sum |terms|
+   * of the fitted curvature's sign test; margin_round = min distance (in gears) of the fitted
+   * vertex + 1/2 to an integer (the rounding to the nearest gear) */
+  double margin_rel, margin_round;
 } or_gear_result;
 
 static uint64_t or_splitmix(uint64_t z) {
@@ -844,7 +916,14 @@ typedef struct {
   double val[256];
   int32_t probed[256];
   int32_t count;
+  double margin_rel, margin_round;
 } or_line;
+
+static void or_gap(or_line* L, double a, double b) {
+  const double m = fabs(a) > fabs(b) ? fabs(a) : fabs(b);
+  const double g = m > 0.0 ? fabs(a - b) / m : INFINITY;
+  if (g < L->margin_rel) L->margin_rel = g;
+}
 
 static double or_eval(or_line* L, int32_t g) {
   if (!L->probed[g]) {
@@ -863,11 +942,13 @@ static int32_t or_line_search(or_line* L, int32_t start, int32_t n) {
   for (int32_t d = 1;; d *= 2) { /* bracket, low side */
     const int32_t g = start - d;
     if (g <= 0) { lo = 0; break; }
+    or_gap(L, or_eval(L, g), o0);
     if (or_eval(L, g) > o0) { lo = g; break; }
   }
   for (int32_t d = 1;; d *= 2) { /* high side */
     const int32_t g = start + d;
     if (g >= n - 1) { hi = n - 1; break; }
+    or_gap(L, or_eval(L, g), o0);
     if (or_eval(L, g) > o0) { hi = g; break; }
   }
   /* discrete golden-section on [lo, hi] */
@@ -881,6 +962,7 @@ static int32_t or_line_search(or_line* L, int32_t start, int32_t n) {
       if (x1 - a >= b - x2) x1 = x2 - 1; else x2 = x1 + 1;
     }
     if (x1 <= a || x2 >= b || x1 >= x2) break;
+    or_gap(L, or_eval(L, x1), or_eval(L, x2));
     if (or_eval(L, x1) < or_eval(L, x2)) b = x2; else a = x1;
   }
   if (b - a <= 2)
@@ -890,6 +972,8 @@ static int32_t or_line_search(or_line* L, int32_t start, int32_t n) {
   int32_t best = -1;
   for (int32_t g = 0; g < n; ++g)
     if (L->probed[g] && (best < 0 || L->val[g] < L->val[best])) best = g;
+  for (int32_t g = 0; g < n; ++g)
+    if (L->probed[g] && g != best) or_gap(L, L->val[g], L->val[best]);
   int32_t pick[5], m = 0;
   for (int32_t d = 0; d < n && m < 5; ++d) { /* distance d, lower gear first */
     if (best - d >= 0 && L->probed[best - d] && m < 5) pick[m++] = best - d;
@@ -918,8 +1002,19 @@ static int32_t or_line_search(or_line* L, int32_t start, int32_t n) {
   const double dB = M[0][0] * (r[1] * M[2][2] - M[1][2] * r[2]) - r[0] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
                     M[0][2] * (M[1][0] * r[2] - r[1] * M[2][0]);
   const double A = dA / det, B = dB / det;
+  {
+    const double terms = fabs(r[0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1])) + fabs(M[0][1] * (r[1] * M[2][2] - M[1][2] * r[2])) +
+                         fabs(M[0][2] * (r[1] * M[2][1] - M[1][1] * r[2]));
+    const double m = terms > 0.0 ? fabs(dA) / terms : INFINITY;
+    if (m < L->margin_rel) L->margin_rel = m;
+  }
   if (!(A > 0.0)) return best;
   double gv = c0 - B / (2.0 * A);
+  {
+    const double f = gv + 0.5 - floor(gv + 0.5);
+    const double m = f < 1.0 - f ? f : 1.0 - f;
+    if (m < L->margin_round) L->margin_round = m;
+  }
   int32_t g = (int32_t)floor(gv + 0.5);
   if (g < gmin) g = gmin;
   if (g > gmax) g = gmax;
@@ -934,6 +1029,7 @@ int oracle_gear_search(const or_gear_workload* w, const double* sm_mhz, int32_t 
   or_line L;
   memset(&L, 0, sizeof(L));
   L.w = w; L.sm = sm_mhz; L.mem = mem_mhz; L.n_sm = n_sm; L.n_mem = n_mem; L.cap = cap;
+  L.margin_rel = L.margin_round = INFINITY;
   L.dom = 1; L.other = pred_sm; /* memory first */
   const int32_t gm = or_line_search(&L, pred_mem, n_mem);
   out->probes_mem = L.count;
@@ -945,6 +1041,8 @@ int oracle_gear_search(const or_gear_workload* w, const double* sm_mhz, int32_t 
   out->sm_gear = gs;
   out->mem_gear = gm;
   out->objective = oracle_gear_objective(w, sm_mhz, n_sm, mem_mhz, n_mem, cap, gs, gm);
+  out->margin_rel = L.margin_rel;
+  out->margin_round = L.margin_round;
   return 0;
 }
 int oracle_sizeof_gear(void) { return (int)(sizeof(or_gear_workload) * 1000 + sizeof(or_gear_result)); }

@@ -100,3 +100,24 @@ def test_config2_accuracy_context():
         errs.append(abs(d.period - t) / t)
     errs = np.array(errs)
     assert np.mean(errs < 0.05) >= 0.6
+
+
+def test_given_candidates_and_forced_best_reproduce_alg1():
+    # the parity harness's hooks: Alg. 1 from line 6 on a given candidate list (its own) and
+    # with Tcand_opt forced to its own argmin give back exactly the same result
+    x = tg.generate_host(tg.CFG2, 5, 1)[0]
+    p = O.params_for(tg.CFG2)
+    d = O.detect(x, p)
+    assert d.status == O.TRACE_OK
+    g = O.detect(x, p, given_k=d.cand_k)
+    f = O.detect(x, p, force_kb=d.best_bin)
+    for e in (g, f):
+        assert (e.period, e.best_bin, e.local_lo, e.local_hi) == (d.period, d.best_bin, d.local_lo, d.local_hi)
+        assert e.cand_err == d.cand_err and np.array_equal(e.local_err, d.local_err)
+        assert np.array_equal(e.local_margin, d.local_margin)
+    assert min(d.cand_margin + list(d.local_margin)) == d.margins["d_cem"]
+    # forcing another candidate moves the local range to that candidate's bin
+    if d.n_candidates > 1:
+        other = [k for k in d.cand_k if k != d.best_bin][0]
+        e = O.detect(x, p, force_kb=other)
+        assert e.best_bin == other and (e.local_lo, e.local_hi) == O.local_range(8192, other, 10, 4096)

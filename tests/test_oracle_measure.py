@@ -23,7 +23,7 @@ def test_stationary_stops_after_one_round():
     x = tg.generate_host(tg.CFG1)[0]
     m = O.measure(x, O.params_for(tg.CFG1), 1024)
     assert m == dict(status=O.TRACE_OK, t_iter=37, rounds=1, samples=1024, measure_start=1024, measure_end=1061,
-                     err_iter=m["err_iter"])
+                     err_iter=m["err_iter"], amb=False)
 
 
 @pytest.mark.parametrize("L0", [20, 33])

@@ -136,3 +136,13 @@ def test_local_range_matches_paper_fractional_formula(N):
         if abs(hi_f - round(hi_f)) > 1e-9:
             assert hi == min(int(np.floor(hi_f)), N)
         assert lo <= N // k <= hi  # the candidate itself is always in its local range
+
+
+def test_order_margin_of_tied_peaks():
+    # two candidates with equal power: their rank order (and, for a shared L, the dedupe) is a
+    # tie -- d_order = 0 (Z27); well-separated powers give the relative gap
+    N = 1024
+    r = O.candidates(_hand_spectrum(N, {20: 1.0, 45: 1.0}), O.Params(N, min_period=4, max_period=512))
+    assert r.n_candidates == 2 and r.d_order == 0.0
+    r = O.candidates(_hand_spectrum(N, {20: 1.0, 45: 0.8}), O.Params(N, min_period=4, max_period=512))
+    assert r.d_order == pytest.approx(0.2, rel=1e-12)

@@ -118,3 +118,44 @@ def test_band_only_dft_same_values():
     a = O.detect(x, O.Params(2048, 1, min_period=10, max_period=400))
     b = O.detect(x, O.Params(2048, 1, min_period=10, max_period=400, dft_band_only=True))
     assert a.period == b.period and a.cand_L == b.cand_L and a.error == b.error and a.margins == b.margins
+
+
+def _fp32_rounding_is_clear(v64: float, rel=1e-12) -> bool:
+    """False when v lies within rel of an fp32 rounding boundary (a midpoint between two
+    adjacent fp32 values): there a rounding-once claim cannot be checked bit for bit."""
+    r = np.float32(v64)
+    if not np.isfinite(r) or v64 == 0.0:
+        return True
+    up = np.nextafter(r, np.float32(np.inf))
+    dn = np.nextafter(r, np.float32(-np.inf))
+    mids = [(float(r) + float(up)) / 2, (float(r) + float(dn)) / 2]
+    return min(abs(v64 - m) for m in mids) > rel * abs(v64)
+
+
+@pytest.mark.parametrize("F,weights", [(1, None), (3, None), (3, (1.0, 0.5, 2.0)), (2, (0.25, 1.0))])
+def test_composite_is_the_exact_definition_rounded_once(F, weights):
+    """Z23: y[n] is the exact value of the definition (Z1) sum_c w_c (x_c[n] - mu_c)
+    / sigma_c rounded to fp32 once. Reference: a 50-digit decimal evaluation of the
+    definition (no binary floating point in it), compared bit for bit wherever the exact
+    value is not within 1e-12 of an fp32 rounding boundary."""
+    from decimal import Decimal, getcontext
+    getcontext().prec = 50
+    rng = np.random.default_rng(F + (0 if weights is None else 7))
+    N = 257
+    x = np.round(rng.uniform(0, 300, (F, N)) + 40 * np.sin(np.arange(N) * 0.07), 1).astype(np.float32)
+    y, _, _, _ = O.composite(x, weights=weights)
+    w = [Decimal(float(np.float32(v))) for v in (weights or (1.0,) * F)]
+    cols = []
+    for c in range(F):
+        xs = [Decimal(float(v)) for v in x[c]]
+        mu = sum(xs) / N
+        sigma = (sum((v - mu) ** 2 for v in xs) / N).sqrt()
+        cols.append([(v - mu) / sigma * w[c] for v in xs])
+    checked = 0
+    for n in range(N):
+        exact = float(sum(col[n] for col in cols))  # correctly rounded to fp64 (50 digits first)
+        if not _fp32_rounding_is_clear(exact):
+            continue
+        assert y[n] == np.float32(exact), (n, y[n], exact)
+        checked += 1
+    assert checked >= N - 2
