@@ -140,6 +140,19 @@ int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_p
                                gpoeo_detail* detail, void* workspace, size_t workspace_bytes, void* stream,
                                void* const* phase_events);
 
+/* Debug/parity surface of Alg. 1 l.14-16: Err(L) of every L of each trace's
+ * evaluated local range [local_lo, local_hi] (Z18), read from the workspace of the last
+ * gpoeo_detect_periods / _ex / _timed call that used it (same p and batch; enqueue it on
+ * that call's stream, after it; the workspace must not have been reused since).
+ *  local_err  DEVICE [batch][gpoeo_local_range_max(p)] fp64: row t holds Err(local_lo + i)
+ *             at column i <= local_hi - local_lo, NaN in the rest of the row and in every
+ *             row whose status is not OK. Asynchronous, allocation-free.
+ * gpoeo_local_range_max: the row length, max over the band's bins of the local-range size
+ * (HOST, pure; 0 if *p is invalid). */
+int64_t gpoeo_local_range_max(const gpoeo_params* p);
+int gpoeo_local_scores(const void* workspace, const gpoeo_params* p, int64_t batch, double* local_err,
+                       void* stream);
+
 /* End-to-end variant over HOST buffers (the e2e path of bench.py):
  *  host_traces  HOST [batch][trace_stride] fp32 (pinned memory gives async overlap);
  *  host_results HOST [batch] gpoeo_result.

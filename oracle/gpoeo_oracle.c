@@ -100,22 +100,34 @@ typedef struct {
  * mem util; Z1 reading: population z-score per channel, weighted sum, sigma=0
  * channel contributes 0; Z23 reading: the expression is evaluated in fp64 and y is
  * rounded to fp32 once):
- *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N),
+ *   mu_c = sum_n x_c[n] / N,  sigma_c = sqrt(sum_n (x_c[n] - mu_c)^2 / N)  (fp64, full accuracy),
  *   y[n] = fp32( sum_c a_c (x_c[n] - mu_c) ),  a_c = w_c / sigma_c
  * (the scale a_c is formed once per channel, products and sums in channel order, no FMA).
  * Returns 1 if every channel is constant. mu/sigma may be NULL. */
+/* s + c += v with the rounding error of every addition kept in c (Neumaier's variant of
+ * Kahan summation): the sum is accurate to ~1 ulp independently of N. */
+static void neumaier_add(double* s, double* c, double v) {
+  const double t = *s + v;
+  if (fabs(*s) >= fabs(v)) *c += (*s - t) + v;
+  else *c += (v - t) + *s;
+  *s = t;
+}
+
 int oracle_composite(const float* x, int32_t N, int32_t F, const double* w, float* y, double* mu_out,
                      double* sigma_out) {
   double mu[8], sigma[8], a[8];
   int all_const = 1;
   for (int c = 0; c < F; ++c) {
     const float* xc = x + (int64_t)c * N;
-    double s = 0.0;
-    for (int n = 0; n < N; ++n) s += (double)xc[n];
-    mu[c] = s / N;
-    double q = 0.0;
-    for (int n = 0; n < N; ++n) q += ((double)xc[n] - mu[c]) * ((double)xc[n] - mu[c]);
-    sigma[c] = sqrt(q / N);
+    /* both sums to full fp64 accuracy (Neumaier-compensated; a plain running sum loses up
+     * to ~N eps relative at N = 2^16-2^18, enough to move y's rounding: pinned against a
+     * 50-digit evaluation of the definition) */
+    double s = 0.0, cs = 0.0;
+    for (int n = 0; n < N; ++n) neumaier_add(&s, &cs, (double)xc[n]);
+    mu[c] = (s + cs) / N;
+    double q = 0.0, cq = 0.0;
+    for (int n = 0; n < N; ++n) neumaier_add(&q, &cq, ((double)xc[n] - mu[c]) * ((double)xc[n] - mu[c]));
+    sigma[c] = sqrt((q + cq) / N);
     a[c] = sigma[c] > 0.0 ? (w ? w[c] : 1.0) / sigma[c] : 0.0;
     if (sigma[c] > 0.0) all_const = 0;
     if (mu_out) mu_out[c] = mu[c];

@@ -133,6 +133,10 @@ def load():
     lib.gpoeo_gear_search.argtypes = [P, ctypes.c_int64, P, ctypes.c_int32, P, ctypes.c_int32, ctypes.c_double, P, P,
                                       P, P]
     lib.gpoeo_gear_search.restype = ctypes.c_int
+    lib.gpoeo_local_range_max.argtypes = [PP]
+    lib.gpoeo_local_range_max.restype = ctypes.c_int64
+    lib.gpoeo_local_scores.argtypes = [P, PP, ctypes.c_int64, P, P]
+    lib.gpoeo_local_scores.restype = ctypes.c_int
     lib.gpoeo_read_counters.argtypes = [P, PP, ctypes.c_int64, ctypes.POINTER(GpoeoCounters), P]
     lib.gpoeo_read_counters.restype = ctypes.c_int
     lib.gpoeo_status_string.argtypes = [ctypes.c_int]
@@ -395,6 +399,18 @@ def gear_search(workloads: np.ndarray, sm_mhz, mem_mhz, cap: float, pred_sm, pre
                                ctypes.c_void_p(pm.data_ptr()), ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
     _check(rc, "gpoeo_gear_search")
     return out.cpu().numpy().view(GEAR_RESULT_DTYPE)
+
+
+def local_scores(workspace, p: GpoeoParams, batch: int, stream=None):
+    """gpoeo_local_scores: [batch][local_range_max] fp64 device tensor of the local-range
+    Err(L) of the last detect call on `workspace` (NaN-padded)."""
+    import torch
+    lib = load()
+    ml = int(lib.gpoeo_local_range_max(ctypes.byref(p)))
+    out = torch.empty((batch, max(ml, 1)), dtype=torch.float64, device=workspace.device)
+    _check(lib.gpoeo_local_scores(ctypes.c_void_p(workspace.data_ptr()), ctypes.byref(p), batch,
+                                  ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)), "gpoeo_local_scores")
+    return out
 
 
 def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:

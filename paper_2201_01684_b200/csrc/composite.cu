@@ -1,14 +1,15 @@
-// composite.cu — row a1: the composite detection signal (reading Z1/Z23).
+// composite.cu — row a1: the composite detection signal (readings Z1/Z23).
 //
 //   mu_c = sum_n x_c[n] / N,   sigma_c^2 = sum_n (x_c[n] - x_c[0])^2 / N - (mu_c - x_c[0])^2
-//   m_c = fp32(mu_c),  s_c = fp32(w_c / sigma_c)  (channels with sigma_c == 0 skipped)
-//   y[n] = fp32 channel-order sum of s_c (x_c[n] - m_c), each op rounded to nearest (Z23b)
+//   a_c = w_c / sigma_c  (fp64, once per channel; channels with sigma_c == 0 skipped)
+//   y[n] = fp32( fp64 channel-order sum of a_c (x_c[n] - mu_c) )  -- rounded once (Z23)
 //
 // One CTA per trace, 512 threads. Pass 1 reads x once with 128-bit loads and forms the
 // fp64 sums (shifted by x_c[0] so the variance does not cancel); pass 2 re-reads x (an
-// L2 hit: the trace was just streamed) and writes y with 128-bit stores. The fp32 ops use
-// explicit _rn intrinsics (no FMA), so y is bit-identical to the oracle's whenever m_c and
-// s_c round to the same fp32 values (the fp64 statistics agree to ~1e-16).
+// L2 hit: the trace was just streamed) and writes y with 128-bit stores. The fp64 ops use
+// explicit _rn intrinsics (no FMA), the oracle's operation sequence, so y is bit-identical
+// to the oracle's unless the fp64 value sits within the statistics' last-bit difference of
+// an fp32 rounding boundary (<= 1 ulp then; the statistics are summed in another order).
 #include "gpoeo_internal.cuh"
 
 namespace gpoeo {
@@ -36,13 +37,16 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
   if (plan.row_n) N = plan.row_n[t];  // ragged batch: this row's length
   const float* xt = x + (plan.row_idx ? (int64_t)plan.row_idx[t] : t) * stride;
   const int64_t cs = plan.cstride;     // channel c of the trace at xt + c * cs
-  float m[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
+  // 128-bit path only when every channel row and the output row stay 16-B aligned (a ragged
+  // row's N need not share the plan's strides' alignment)
+  const bool vec = (N & 3) == 0 && (cs & 3) == 0 && (plan.ystride & 3) == 0 && (stride & 3) == 0;
+  double m[GPOEO_MAX_FEATURES], a[GPOEO_MAX_FEATURES];
   bool all_const = true;
   for (int c = 0; c < F; ++c) {
     const float* xc = xt + (int64_t)c * cs;
     const double x0 = (double)__ldg(xc);
     double s = 0.0, q = 0.0;
-    if ((N & 3) == 0) {
+    if (vec) {
       const float4* x4 = reinterpret_cast<const float4*>(xc);
 #pragma unroll 8
       for (int i = threadIdx.x; i < N / 4; i += kCompThreads) {
@@ -67,32 +71,33 @@ __global__ void __launch_bounds__(kCompThreads) composite_kernel(const float* __
     double var = q / (double)N - dm * dm;
     if (!(var > 0.0)) var = 0.0;
     const double sigma = sqrt(var);
-    m[c] = __double2float_rn(mu);
-    a[c] = sigma > 0.0 ? __double2float_rn((double)plan.w[c] / sigma) : 0.f;
+    m[c] = mu;
+    a[c] = sigma > 0.0 ? (double)plan.w[c] / sigma : 0.0;
     if (sigma > 0.0) all_const = false;
   }
   if (threadIdx.x == 0) status[t] = all_const ? GPOEO_TRACE_CONSTANT : GPOEO_TRACE_OK;
   float* yt = y + t * plan.ystride;
-  if ((N & 3) == 0) {
+  if (vec) {
 #pragma unroll 4
     for (int i = threadIdx.x; i < N / 4; i += kCompThreads) {
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
       for (int c = 0; c < F; ++c) {
-        if (a[c] == 0.f) continue;
+        if (a[c] == 0.0) continue;
         float4 xv = __ldg(reinterpret_cast<const float4*>(xt + (int64_t)c * cs) + i);
-        v[0] = __fadd_rn(v[0], __fmul_rn(a[c], __fsub_rn(xv.x, m[c])));
-        v[1] = __fadd_rn(v[1], __fmul_rn(a[c], __fsub_rn(xv.y, m[c])));
-        v[2] = __fadd_rn(v[2], __fmul_rn(a[c], __fsub_rn(xv.z, m[c])));
-        v[3] = __fadd_rn(v[3], __fmul_rn(a[c], __fsub_rn(xv.w, m[c])));
+        v[0] = __dadd_rn(v[0], __dmul_rn(a[c], __dsub_rn((double)xv.x, m[c])));
+        v[1] = __dadd_rn(v[1], __dmul_rn(a[c], __dsub_rn((double)xv.y, m[c])));
+        v[2] = __dadd_rn(v[2], __dmul_rn(a[c], __dsub_rn((double)xv.z, m[c])));
+        v[3] = __dadd_rn(v[3], __dmul_rn(a[c], __dsub_rn((double)xv.w, m[c])));
       }
-      reinterpret_cast<float4*>(yt)[i] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(yt)[i] = make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]),
+                                                     __double2float_rn(v[2]), __double2float_rn(v[3]));
     }
   } else {
     for (int i = threadIdx.x; i < N; i += kCompThreads) {
-      float v = 0.f;
+      double v = 0.0;
       for (int c = 0; c < F; ++c)
-        if (a[c] != 0.f) v = __fadd_rn(v, __fmul_rn(a[c], __fsub_rn(__ldg(xt + (int64_t)c * cs + i), m[c])));
-      yt[i] = v;
+        if (a[c] != 0.0) v = __dadd_rn(v, __dmul_rn(a[c], __dsub_rn((double)__ldg(xt + (int64_t)c * cs + i), m[c])));
+      yt[i] = __double2float_rn(v);
     }
   }
 }

@@ -287,8 +287,9 @@ static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_para
   R.gsig = take(sizeof(float) * (size_t)B * (size_t)((p->n_samples + 3) & ~3));
   R.gres = take(sizeof(gpoeo_result) * (size_t)B);
   R.gdet = take(sizeof(gpoeo_detail) * (size_t)B);
-  // one chunk of suffixes: at most B rows of at most N samples; local ranges bounded by the band
-  gpoeo_params q = suffix_params(p, p->n_samples);
+  // one chunk of suffixes: at most B rows of at most N samples (rows padded to a multiple of 4
+  // floats, so the chunk's row length may reach N rounded up); local ranges bounded by the band
+  gpoeo_params q = suffix_params(p, (p->n_samples + 3) & ~3);
   Plan pl = make_plan(&q, B);
   pl.max_local = (int64_t)q.max_period - q.min_period + 1;
   R.gws = take(layout(pl).total);
@@ -454,6 +455,25 @@ int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_p
     return GPOEO_ERR_INVALID_ARGUMENT;  // item slots are int32: split the batch
   if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
   return run_detect(traces, pl, L, workspace, results, detail, static_cast<cudaStream_t>(stream), phase_events);
+}
+
+int64_t gpoeo_local_range_max(const gpoeo_params* p) {
+  if (validate(p) != GPOEO_OK) return 0;
+  return make_plan(p, 0).max_local;
+}
+
+int gpoeo_local_scores(const void* workspace, const gpoeo_params* p, int64_t batch, double* local_err,
+                       void* stream) {
+  int v = validate(p);
+  if (v != GPOEO_OK) return v;
+  if (batch < 0 || (batch > 0 && !local_err)) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (!workspace) return GPOEO_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
+  if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
+  const Plan pl = make_plan(p, batch);
+  const Work w = carve(pl, layout(pl), const_cast<void*>(workspace));
+  CK(launch_local_scores(pl, w, local_err, static_cast<cudaStream_t>(stream)));
+  return GPOEO_OK;
 }
 
 int gpoeo_detect_periods(const float* traces, int64_t batch, const gpoeo_params* p, gpoeo_result* results,

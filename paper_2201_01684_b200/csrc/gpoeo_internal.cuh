@@ -164,6 +164,7 @@ cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* 
 cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
                          int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);
+cudaError_t launch_local_scores(const Plan& p, Work w, double* out, cudaStream_t s);
 
 // Gear local search (gear.cu)
 cudaError_t launch_gear_search(const gpoeo_gear_workload* w, int64_t n, const double* sm, int32_t n_sm,

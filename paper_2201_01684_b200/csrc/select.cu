@@ -105,6 +105,23 @@ __global__ void final_kernel(Plan pc, Work w, gpoeo_result* __restrict__ res, gp
   }
 }
 
+// Debug surface (gpoeo_local_scores): the local-range scores of trace t into row t of a
+// [batch][ml] array, NaN-padded.
+__global__ void local_scores_kernel(Plan pc, Work w, double* __restrict__ out, int64_t ml) {
+  const int64_t t = blockIdx.x;
+  const int32_t st = w.status[t];
+  const int64_t cnt = st == GPOEO_TRACE_OK ? (int64_t)w.local_hi[t] - w.local_lo[t] + 1 : 0;
+  const double* le = w.local_err + (st == GPOEO_TRACE_OK ? w.local_base[t] : 0);
+  for (int64_t i = threadIdx.x; i < ml; i += blockDim.x)
+    out[t * ml + i] = i < cnt ? le[i] : __longlong_as_double(0x7ff8000000000000ll);
+}
+
+cudaError_t launch_local_scores(const Plan& p, Work w, double* out, cudaStream_t s) {
+  if (p.batch == 0 || p.max_local == 0) return cudaSuccess;
+  local_scores_kernel<<<(unsigned)p.batch, 256, 0, s>>>(p, w, out, p.max_local);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
   select_kernel<<<(unsigned)((p.batch + 127) / 128), 128, 0, s>>>(p, w);

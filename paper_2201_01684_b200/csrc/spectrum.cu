@@ -692,7 +692,7 @@ __device__ __forceinline__ void prefetch_half(const float* xt, int q) {
 // per 2-CTA cluster, one trace at a time per cluster:
 //   A  stats: CTA q reads quarter blocks {q, 2+q} of every channel once (HBM, or L2 when
 //      prefetched), fp64 sums shifted by x_c[0]; partials exchanged through DSMEM.
-//   B  signal: re-reads the same blocks (L2), y = fp32 channel sum of s_c (x_c - m_c) (Z23b),
+//   B  signal: re-reads the same blocks (L2), y = fp32(fp64 channel sum of a_c (x_c - mu_c)) (Z23),
 //      writes y once when the scorer needs it (never in spectral-only mode), and builds
 //      the DIF halves a_0[j] = z[j] + z[j + n2], a_1[j] = (z[j] - z[j + n2]) W^j straight
 //      into the two CTAs' shared memory; then prefetches its half of the next trace to L2.
@@ -774,7 +774,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     }
     cluster.sync();
     bool all_const = true;
-    float m[F], a[F];
+    double m[F], a[F];
 #pragma unroll
     for (int c = 0; c < F; ++c) {
       const double x0 = (double)__ldg(xt + (int64_t)c * kN);
@@ -785,29 +785,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       double var = qq / (double)kN - dm * dm;
       if (!(var > 0.0)) var = 0.0;
       const double sigma = sqrt(var);
-      m[c] = __double2float_rn(mu);
-      a[c] = sigma > 0.0 ? __double2float_rn((double)p.w[c] / sigma) : 0.f;
+      m[c] = mu;
+      a[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
       if (sigma > 0.0) all_const = false;
     }
     // ---- B: signal + DIF split into the two CTAs' buffers ------------------------------
+    // y = fp32(fp64 channel-order sum of a_c (x_c - mu_c)), each fp64 op rounded to nearest,
+    // no FMA: the oracle's O1 sequence (Z23)
     float* yt = y_out ? y_out + t * (int64_t)kN : nullptr;
 #pragma unroll 4
     for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
       const int j = q * (kn2 / 2) + jj;
-      float ya0 = 0.f, ya1 = 0.f, yb0 = 0.f, yb1 = 0.f;
+      double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
 #pragma unroll
       for (int c = 0; c < F; ++c) {
-        if (a[c] == 0.f) continue;
+        if (a[c] == 0.0) continue;
         const float* xc = xt + (int64_t)c * kN;
         const float2 xa = __ldg(reinterpret_cast<const float2*>(xc + 2 * j));
         const float2 xb = __ldg(reinterpret_cast<const float2*>(xc + 2 * j + kn));
-        ya0 = __fadd_rn(ya0, __fmul_rn(a[c], __fsub_rn(xa.x, m[c])));
-        ya1 = __fadd_rn(ya1, __fmul_rn(a[c], __fsub_rn(xa.y, m[c])));
-        yb0 = __fadd_rn(yb0, __fmul_rn(a[c], __fsub_rn(xb.x, m[c])));
-        yb1 = __fadd_rn(yb1, __fmul_rn(a[c], __fsub_rn(xb.y, m[c])));
+        ya0 = __dadd_rn(ya0, __dmul_rn(a[c], __dsub_rn((double)xa.x, m[c])));
+        ya1 = __dadd_rn(ya1, __dmul_rn(a[c], __dsub_rn((double)xa.y, m[c])));
+        yb0 = __dadd_rn(yb0, __dmul_rn(a[c], __dsub_rn((double)xb.x, m[c])));
+        yb1 = __dadd_rn(yb1, __dmul_rn(a[c], __dsub_rn((double)xb.y, m[c])));
       }
-      const float2 za = make_float2(ya0, ya1);
-      const float2 zb = make_float2(yb0, yb1);
+      const float2 za = make_float2(__double2float_rn(ya0), __double2float_rn(ya1));
+      const float2 zb = make_float2(__double2float_rn(yb0), __double2float_rn(yb1));
       if (yt) {
         reinterpret_cast<float2*>(yt)[j] = za;
         reinterpret_cast<float2*>(yt + kn)[j] = zb;
@@ -1103,9 +1105,14 @@ struct BandView {
 
 __device__ __forceinline__ void band_bins_of(const Plan& p, bool all, int* kb0, int* kb1) {
   const int n = p.N / 2;
-  if (all || p.k_lo > p.k_hi) {
+  if (all) {
     *kb0 = 0;
     *kb1 = n;
+    return;
+  }
+  if (p.k_lo > p.k_hi) {  // empty band (Z21): no bin is read, the status is INSUFFICIENT
+    *kb0 = 0;
+    *kb1 = -1;
     return;
   }
   *kb0 = p.k_lo - 1 < 0 ? 0 : p.k_lo - 1;
@@ -1174,7 +1181,8 @@ __global__ void __launch_bounds__(kBandT) spectrum_band_kernel(Plan pc, const fl
 // ragged batch p is sized for the longest row: its band (N/L_min) bounds every row's.
 static int band_slots(const Plan& p, bool all) {
   const int n = p.N / 2;
-  if (all || p.k_lo > p.k_hi) return n + 1;
+  if (all) return n + 1;
+  if (p.k_lo > p.k_hi && !p.row_n) return 1;  // empty band: nothing is evaluated
   const int kb0 = p.k_lo - 1 < 0 ? 0 : p.k_lo - 1;
   const int khi = p.row_n ? p.N / p.Lmin : p.k_hi;  // rows clip L_max to N_j/2: bands may start at 1
   const int kb1 = khi + 1 > n ? n : khi + 1;

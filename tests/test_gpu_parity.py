@@ -1,14 +1,16 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
 
-Bars (BASELINE.json north star):
-  * detected periods, candidate lists, local ranges, statuses: bit-exact;
+Bars (BASELINE.json north star; the harness is tests/parity.py):
+  * detected periods, candidate lists, best bins, local ranges, statuses: bit-exact;
   * spectra: normwise max|P_gpu - P_ref| <= 1e-4 max P_ref (Z29);
-  * Alg. 2 scores: |Err_gpu - Err_ref| <= 1e-4 max(Err_ref, 1e-6) (Z30);
-  * composite signal: bit-identical except where the fp64 value sits within rounding of an
-    fp32 boundary (<= 1 ulp, a vanishing fraction).
-Where the oracle reports a decision margin below what the precision difference between the
-two sides can move (Z27), several answers are correct: those traces are counted, must be
-rare, and are checked for validity instead of equality.
+  * Alg. 2 scores of every candidate AND every local L: |Err_gpu - Err_ref| <= 1e-4 max(Err_ref, 1e-6)
+    (Z30);
+  * composite signal: the fp64 expression rounded once on both sides (Z23) -- bit-identical
+    except where the two sides' fp64 statistics (summed in different orders) straddle an fp32
+    rounding boundary: <= 1 ulp there, counted (expected ~1e-8 of the samples).
+Where the oracle records a decision margin below what the precision difference between the
+two sides can move (Z27), several answers are correct: the GPU's answer is then checked for
+validity against the oracle (parity.py), and every such exclusion is counted with its reason.
 """
 import numpy as np
 import pytest
@@ -17,6 +19,7 @@ import torch  # noqa: E402
 
 import oracle as O  # noqa: E402
 import paper_2201_01684_b200 as g  # noqa: E402
+import parity as PH  # noqa: E402
 import tracegen as tg  # noqa: E402
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
@@ -35,44 +38,16 @@ def _to_dev(x: np.ndarray):
 
 def _detect(x: np.ndarray, p):
     res, det, ws = g.detect_periods(_to_dev(x), p, detail=True)
+    loc = g.local_scores(ws, p, x.shape[0])
     torch.cuda.synchronize()
-    return g.results_numpy(res), g.detail_numpy(det), ws
+    return g.results_numpy(res), g.detail_numpy(det), loc.cpu().numpy(), ws
 
 
-def _compare(res, det, ods, label=""):
-    """Compare GPU records with oracle Detections; returns (n_exact, n_ambiguous)."""
-    n_amb = 0
-    for i, d in enumerate(ods):
-        r, q = res[i], det[i]
-        assert r["status"] == d.status, (label, i, r["status"], d.status)
-        if d.status == O.TRACE_CONSTANT:
-            continue
-        amb = d.ambiguous()
-        if amb:
-            n_amb += 1
-        if d.status != O.TRACE_OK:
-            assert r["n_candidates"] == 0 and r["period"] == -1
-            continue
-        if not amb or d.margins["d_thr"] >= 1e-5 and d.margins["d_peak"] >= 1e-5 and d.margins["d_rank"] >= 1e-5:
-            nc = d.n_candidates
-            assert q["n_candidates"] == nc, (label, i)
-            assert list(q["cand_k"][:nc]) == d.cand_k, (label, i)
-            assert list(q["cand_L"][:nc]) == d.cand_L, (label, i)
-            for c in range(nc):
-                ref = d.cand_err[c]
-                assert abs(q["cand_err"][c] - ref) <= 1e-4 * max(ref, 1e-6), (label, i, c, q["cand_err"][c], ref)
-        if amb:
-            # validity: the GPU answer lies in its own local range and is one of the oracle's near-best
-            assert q["local_lo"] <= r["period"] <= q["local_hi"]
-            continue
-        assert q["best_bin"] == d.best_bin, (label, i)
-        assert (q["local_lo"], q["local_hi"]) == (d.local_lo, d.local_hi), (label, i)
-        assert r["period"] == d.period, (label, i, r["period"], d.period, d.margins)
-        assert r["best_candidate"] == d.best_candidate
-        assert abs(q["best_err"] - d.error) <= 1e-4 * max(d.error, 1e-6), (label, i, q["best_err"], d.error)
-        assert r["period_s"] == np.float32(d.period * 1.0)
-    assert n_amb <= max(1, len(ods) // 10), (label, n_amb)
-    return len(ods) - n_amb, n_amb
+def _check(x, op, got, label, ods=None, max_excluded_frac=0.1):
+    """Alg. 1 records of the GPU (res, det, loc) against the oracle on x under op."""
+    res, det, loc = got[:3]
+    ods = ods if ods is not None else O.detect_batch(x, op)
+    return PH.check_batch(x, op, res, det, loc, ods, label, max_excluded_frac)
 
 
 # ---------------------------------------------------------------------------------------
@@ -98,12 +73,17 @@ def test_composite_signal_matches_oracle(N, F):
     p = g.default_params(N, F)
     _, sig = g.power_spectrum(_to_dev(x), p)
     sig = sig.cpu().numpy()
+    n_off = 0
     for b in range(B):
         y, _, _, _ = O.composite(x[b])
         diff = sig[b].view(np.int32).astype(np.int64) - y.view(np.int32).astype(np.int64)
-        # identical fp32 expression (Z23b) from fp64 statistics rounded once: bit-identical
-        # unless mu or w/sigma sat within ~1e-16 of an fp32 rounding boundary
-        assert np.count_nonzero(diff) == 0, np.count_nonzero(diff)
+        # the same fp64 expression rounded once (Z23) from fp64 statistics summed in another
+        # order: bit-identical unless the value sits within their last-bit difference of an
+        # fp32 rounding boundary -- then 1 ulp
+        assert np.abs(diff).max() <= 1, np.abs(diff).max()
+        n_off += np.count_nonzero(diff)
+    print(f"[composite N={N} F={F}] samples={B * N} off-by-1ulp={n_off}")
+    assert n_off <= max(2, B * N // 10**6)
 
 
 @pytest.mark.parametrize("N", [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768, 65536])
@@ -209,34 +189,31 @@ def test_similarity_exact_zero_on_periodic():
 
 def test_detect_config1():
     x = tg.generate_host(tg.CFG1)
-    res, det, _ = _detect(x, g.params_for(tg.CFG1))
-    assert res[0]["period"] == 37 and res[0]["status"] == 0
-    _compare(res, det, [O.detect(x[0], O.params_for(tg.CFG1))], "cfg1")
+    got = _detect(x, g.params_for(tg.CFG1))
+    assert got[0][0]["period"] == 37 and got[0][0]["status"] == 0
+    t = _check(x, O.params_for(tg.CFG1), got, "cfg1")
+    assert t.exact == 1
 
 
 def test_detect_config2_all_71():
     x = tg.generate_host(tg.CFG2)
-    res, det, _ = _detect(x, g.params_for(tg.CFG2))
-    ods = O.detect_batch(x, O.params_for(tg.CFG2))
-    exact, amb = _compare(res, det, ods, "cfg2")
-    assert exact >= 68
+    t = _check(x, O.params_for(tg.CFG2), _detect(x, g.params_for(tg.CFG2)), "cfg2")
+    assert t.exact >= 69
 
 
 def test_detect_config3_shape_subset():
     spec = tg.CFG3
     idx = [0, 1, 2, 3, 5, 8, 13, 21, 34, 55, 89, 144, 233, 377, 610, 987]
     x = np.stack([tg.generate_host(spec, i, 1)[0] for i in idx])
-    res, det, _ = _detect(x, g.params_for(spec))
-    ods = O.detect_batch(x, O.params_for(spec, dft_band_only=True))
-    _compare(res, det, ods, "cfg3")
+    _check(x, O.params_for(spec, dft_band_only=True), _detect(x, g.params_for(spec)), "cfg3")
 
 
-def test_detect_config5_shape_subset():
+def test_detect_config5_first16():
+    # BASELINE config 5 (2^18 samples, mid-trace period shift, harmonic aliasing): its first
+    # 16 traces, every decision and score against the oracle (SURVEY 8(d) subset)
     spec = tg.CFG5
-    x = np.stack([tg.generate_host(spec, i, 1)[0] for i in (0, 1)])
-    res, det, _ = _detect(x, g.params_for(spec))
-    ods = O.detect_batch(x, O.params_for(spec, dft_band_only=True))
-    _compare(res, det, ods, "cfg5")
+    x = tg.generate_host(spec, 0, 16)
+    _check(x, O.params_for(spec, dft_band_only=True), _detect(x, g.params_for(spec)), "cfg5")
 
 
 def test_edge_cases_statuses_and_small_n():
@@ -252,12 +229,12 @@ def test_edge_cases_statuses_and_small_n():
     x[4, 0] = np.tile([0, 10], N // 2)               # period 2 (L_min)
     x[4, 1] = np.tile([1, 3], N // 2)              # in phase (anti-phase would cancel)
     p = g.default_params(N, 2, min_period=2, max_period=32)
-    res, det, _ = _detect(x, p)
-    ods = [O.detect(x[b], O.Params(N, 2, min_period=2, max_period=32)) for b in range(5)]
+    got = _detect(x, p)
+    res = got[0]
     assert res[0]["status"] == g.TRACE_CONSTANT and res[0]["period"] == -1
     assert res[1]["status"] == g.TRACE_APERIODIC
     assert res[2]["period"] == 7 and res[4]["period"] == 2
-    _compare(res, det, ods, "edge")
+    _check(x, O.Params(N, 2, min_period=2, max_period=32), got, "edge")
 
 
 @pytest.mark.parametrize("N", [8, 16, 32])
@@ -265,9 +242,7 @@ def test_tiny_n(N):
     rng = np.random.default_rng(N)
     x = np.round(rng.uniform(0, 50, (4, 1, N))).astype(np.float32)
     x[0, 0] = np.tile([1, 5, 2], N)[:N]
-    p = g.default_params(N, 1)
-    res, det, _ = _detect(x, p)
-    _compare(res, det, [O.detect(x[b], O.Params(N, 1)) for b in range(4)], f"tiny{N}")
+    _check(x, O.Params(N, 1), _detect(x, g.default_params(N, 1)), f"tiny{N}")
 
 
 @pytest.mark.parametrize("kw", [dict(max_candidates=1), dict(num_groups=2), dict(num_groups=8), dict(gmm_max_iters=1),
@@ -278,29 +253,29 @@ def test_parameter_variants(kw):
     okw = dict(kw)
     if "min_period" not in kw:
         okw.update(min_period=spec.min_period, max_period=spec.max_period)
-    res, det, _ = _detect(x, g.default_params(spec.n_samples, 3, **({**dict(min_period=spec.min_period,
-                                                                            max_period=spec.max_period), **kw})))
-    ods = O.detect_batch(x, O.Params(spec.n_samples, 3, **okw))
-    _compare(res, det, ods, str(kw))
+    got = _detect(x, g.default_params(spec.n_samples, 3, **({**dict(min_period=spec.min_period,
+                                                                    max_period=spec.max_period), **kw})))
+    _check(x, O.Params(spec.n_samples, 3, **okw), got, str(kw))
 
 
 def test_deterministic_and_batch_order_invariant():
     spec = tg.CFG2.with_(batch=24)
     x = tg.generate_host(spec)
     p = g.params_for(spec)
-    r1, d1, _ = _detect(x, p)
-    r2, d2, _ = _detect(x, p)
-    assert r1.tobytes() == r2.tobytes() and d1.tobytes() == d2.tobytes()
+    r1, d1, l1, _ = _detect(x, p)
+    r2, d2, l2, _ = _detect(x, p)
+    assert r1.tobytes() == r2.tobytes() and d1.tobytes() == d2.tobytes() and l1.tobytes() == l2.tobytes()
     perm = np.random.default_rng(0).permutation(24)
-    r3, d3, _ = _detect(x[perm], p)
+    r3, d3, l3, _ = _detect(x[perm], p)
     assert r3.tobytes() == r1[perm].tobytes() and d3.tobytes() == d1[perm].tobytes()
+    assert l3.tobytes() == l1[perm].tobytes()
 
 
 def test_host_entry_point_matches_device():
     spec = tg.CFG2.with_(batch=40)
     x = tg.generate_host(spec)
     p = g.params_for(spec)
-    r1, _, _ = _detect(x, p)
+    r1 = _detect(x, p)[0]
     pinned = torch.from_numpy(x.reshape(40, -1)).pin_memory()
     r2 = g.detect_periods_host(pinned, p, chunk=7)
     assert r2.tobytes() == r1.tobytes()
@@ -310,7 +285,7 @@ def test_work_counters():
     spec = tg.CFG2.with_(batch=10)
     x = tg.generate_host(spec)
     p = g.params_for(spec)
-    res, det, ws = _detect(x, p)
+    res, det, _, ws = _detect(x, p)
     c = g.read_counters(ws, p, 10)
     assert c["n_candidate_queries"] == int(det["n_candidates"][res["status"] == 0].sum())
     # local queries = the local ranges minus candidates already scored (memoised, as in the oracle)
@@ -332,15 +307,18 @@ def test_full_size_config3_sampled():
     x = torch.empty((B, spec.n_features * spec.n_samples), dtype=torch.float32, device="cuda")
     tg.generate_device(spec, x)
     p = g.params_for(spec)
-    res, det, _ = g.detect_periods(x, p, detail=True)
+    res, det, ws = g.detect_periods(x, p, detail=True)
     torch.cuda.synchronize()
     del x
-    idx = [0, 1, 4242, 31337, 50000, 77777, 99998, 99999]
+    # 64 traces spread over the whole 10^5 batch (first, last, and 60 seeded picks)
+    rng = np.random.default_rng(2024)
+    idx = sorted(set([0, 1, 99998, 99999] + rng.choice(np.arange(2, 99998), 60, replace=False).tolist()))
+    ti = torch.as_tensor(idx, device="cuda")
+    loc = g.local_scores(ws, p, B)[ti].cpu().numpy()
     r = g.results_numpy(res)[idx]
     d = g.detail_numpy(det)[idx]
     xs = np.stack([tg.generate_host(spec, i, 1)[0] for i in idx])
-    ods = O.detect_batch(xs, O.params_for(spec, dft_band_only=True))
-    _compare(r, d, ods, "cfg3-full")
+    _check(xs, O.params_for(spec, dft_band_only=True), (r, d, loc), "cfg3-full")
     allr = g.results_numpy(res)
     assert set(np.unique(allr["status"])) <= {0, 1}
     assert (allr["period"][allr["status"] == 0] >= spec.min_period).all()
@@ -379,19 +357,27 @@ def _major_compare(x, spec, label):
     res, _ = g.detect_major_periods(_to_dev(x), p)
     torch.cuda.synchronize()
     r = g.major_numpy(res)
-    ms = O.major_batch(x, O.params_for(spec, dft_band_only=spec.n_samples > 8192))
+    op = O.params_for(spec, dft_band_only=spec.n_samples > 8192)
+    ms = O.major_batch(x, op)
     n_amb = 0
     for i, m in enumerate(ms):
         assert r[i]["status"] == m.status, (label, i)
         if m.status != O.TRACE_OK:
             assert r[i]["period"] == -1 and r[i]["bin"] == -1
             continue
-        if m.ambiguous(1e-5):
+        if r[i]["bin"] != m.bin:
+            # Z27: only a near-tie of the two largest peaks (or a peak test) may move f_major;
+            # the GPU's bin must then be an in-band peak within 1e-5 P_major of the maximum on
+            # the oracle's own DFT values
+            assert m.ambiguous(), (label, i, r[i]["bin"], m.bin, m.d_major, m.d_peak)
+            y = O.composite(x[i], weights=op.weights)[0]
+            pm, pk, pp = PH._p3(y, int(r[i]["bin"]))
+            eps = O.THR_SPEC * m.power
+            assert pk >= m.power - eps and pk > pm - eps and pk >= pp - eps, (label, i)
             n_amb += 1
-            continue
-        assert r[i]["bin"] == m.bin, (label, i, r[i]["bin"], m.bin, m.d_major)
-        assert r[i]["period"] == m.period
-        assert r[i]["period_s"] == np.float32(m.period_s)
+        assert r[i]["period"] == spec.n_samples // r[i]["bin"]
+        assert r[i]["period_s"] == np.float32(r[i]["period"] * op.sample_interval)
+    print(f"[major {label}] traces={len(ms)} justified-exclusions={n_amb}")
     assert n_amb <= max(1, len(ms) // 10), (label, n_amb)
     return r
 
@@ -459,18 +445,19 @@ def test_non_pow2_detect_matches_oracle(N, F):
     spec = tg.CFG2.with_(batch=12, n_samples=N, n_features=F, period_lo=20.0, period_hi=N / 6, min_period=10,
                          max_period=N // 3)
     x = tg.generate_host(spec)
-    res, det, _ = _detect(x, g.params_for(spec))
-    ods = O.detect_batch(x, O.params_for(spec))
-    _compare(res, det, ods, f"N{N}")
+    _check(x, O.params_for(spec), _detect(x, g.params_for(spec)), f"N{N}")
     _major_compare(x, spec, f"major-N{N}")
 
 
 # ---- Alg. 3 rolling detector (oracle R1, reading R5) ------------------
 
-def _rolling_compare(x, spec, label):
+def _rolling_compare(x, spec, label, weights=None):
     p = g.params_for(spec)
+    if weights is not None:
+        for c, v in enumerate(weights):
+            p.feature_weights[c] = v
     r = g.detect_rolling(_to_dev(x), p)
-    op = O.params_for(spec, dft_band_only=True)
+    op = O.params_for(spec, dft_band_only=True, weights=weights)
     n_amb = 0
     for i in range(x.shape[0]):
         o = O.rolling(x[i], op)
@@ -478,28 +465,20 @@ def _rolling_compare(x, spec, label):
         if o.status != O.TRACE_OK:
             assert r[i]["t_iter"] == -1
             continue
-        whole = O.detect(x[i], op)
-        if whole.ambiguous():
-            n_amb += 1
-            continue
-        assert r[i]["t_init"] == o.t_init, (label, i)
-        assert bool(r[i]["early"]) == o.early and r[i]["n_sub"] == len(o.sub_start), (label, i)
-        # the suffix decisions: ambiguous suffixes (Z27) may legitimately differ
-        y = O.composite(x[i])[0]
-        sub_amb = False
-        for s0, T in zip(o.sub_start, o.sub_period):
-            q = O.Params(len(y) - s0, 1, min_period=spec.min_period, max_period=min(spec.max_period, (len(y) - s0) // 2),
-                         dft_band_only=True)
-            if q.min_period <= q.max_period and O.detect(y[s0:][None], q).ambiguous():
-                sub_amb = True
-        if sub_amb:
-            n_amb += 1
-            continue
-        assert r[i]["t_iter"] == o.t_iter, (label, i, r[i]["t_iter"], o.t_iter, o.sub_period)
         want_next = np.float32(o.smpdur_next * 1.0) if o.smpdur_next >= 0 else np.float32(-1.0)
-        assert r[i]["smpdur_next_s"] == want_next, (label, i, r[i]["smpdur_next_s"], o.smpdur_next)
+        got = (int(r[i]["t_init"]), bool(r[i]["early"]), int(r[i]["n_sub"]), int(r[i]["t_iter"]),
+               float(r[i]["smpdur_next_s"]))
+        want = (o.t_init, o.early, len(o.sub_start), o.t_iter, float(want_next))
+        if got != want:
+            # Z27: only a call whose oracle records a decision margin below the thresholds
+            # (an ambiguous Alg. 1 on the whole trace or a suffix, a line-14 near-tie, Diff
+            # at the threshold) may take another valid trajectory
+            assert o.amb, (label, i, got, want, o.sub_period)
+            n_amb += 1
+            continue
         if np.isfinite(o.diff):
             assert abs(r[i]["diff"] - o.diff) <= 1e-6 * max(1.0, o.diff)
+    print(f"[rolling {label}] traces={x.shape[0]} justified-exclusions={n_amb}")
     assert n_amb <= max(1, x.shape[0] // 5), (label, n_amb)
 
 
@@ -523,19 +502,26 @@ def test_rolling_period_shift():
 
 # ---- Alg. 4 adaptive measurement (oracle M1, reading R6) ----------------
 
-def _measure_compare(x, spec, init, label):
-    r = g.measure_adaptive(_to_dev(x), g.params_for(spec), init)
-    op = O.params_for(spec, dft_band_only=True)
-    bad = []
+def _measure_compare(x, spec, init, label, weights=None):
+    p = g.params_for(spec)
+    if weights is not None:
+        for c, v in enumerate(weights):
+            p.feature_weights[c] = v
+    r = g.measure_adaptive(_to_dev(x), p, init)
+    op = O.params_for(spec, dft_band_only=True, weights=weights)
+    n_amb = 0
     for i in range(x.shape[0]):
         o = O.measure(x[i], op, init)
         got = (int(r[i]["status"]), int(r[i]["t_iter"]), int(r[i]["rounds"]), int(r[i]["samples"]),
                int(r[i]["measure_start"]), int(r[i]["measure_end"]))
         want = (o["status"], o["t_iter"], o["rounds"], o["samples"], o["measure_start"], o["measure_end"])
         if got != want:
-            bad.append((i, got, want))
-    # a near-tie inside any round's Alg. 1 (Z27) may legitimately change the trajectory
-    assert len(bad) <= max(1, x.shape[0] // 8), (label, bad)
+            # Z27: a near-tie inside some round's Alg. 3 call (recorded by the oracle) may
+            # legitimately change the session's trajectory; nothing else may
+            assert o["amb"], (label, i, got, want)
+            n_amb += 1
+    print(f"[measure {label}] sessions={x.shape[0]} justified-exclusions={n_amb}")
+    assert n_amb <= max(1, x.shape[0] // 5), (label, n_amb)
     return r
 
 
@@ -580,16 +566,22 @@ def test_gear_search_matches_oracle():
     ps = rng.integers(0, len(sm), n).astype(np.int32)
     pm = rng.integers(0, len(mem), n).astype(np.int32)
     r = g.gear_search(wl, sm, mem, 0.05, ps, pm)
-    bad = 0
+    n_amb = 0
     for i in range(n):
         w = O.gear_workload(**{k: (int(wl[k][i]) if k == "seed" else float(wl[k][i])) for k in wl.dtype.names})
         o = O.gear_search(w, sm, mem, 0.05, int(ps[i]), int(pm[i]))
         got = (int(r[i]["sm_gear"]), int(r[i]["mem_gear"]), int(r[i]["probes_sm"]), int(r[i]["probes_mem"]))
         if got != (o["sm_gear"], o["mem_gear"], o["probes_sm"], o["probes_mem"]):
-            bad += 1  # only a last-ulp difference of pow() between the two libraries can do this
+            # Z27: the two sides' pow() differ in the last ulps (CUDA libdevice vs glibc), so only
+            # a search decision the oracle took on a relative margin below 1e-12 (two objective
+            # values, or the fitted curvature's sign) or a vertex within 1e-9 of a rounding
+            # boundary may go the other way
+            assert o["margin_rel"] < 1e-12 or o["margin_round"] < 1e-9, (i, got, o)
+            n_amb += 1
             continue
         assert abs(r[i]["objective"] - o["objective"]) <= 1e-12 * abs(o["objective"])
-    assert bad <= 2, bad
+    print(f"[gear] workloads={n} justified-exclusions={n_amb}")
+    assert n_amb <= 4, n_amb
 
 
 def test_rolling_and_measure_non_pow2_weighted():
@@ -597,24 +589,24 @@ def test_rolling_and_measure_non_pow2_weighted():
     spec = tg.CFG2.with_(batch=8, n_samples=3000, period_lo=20.0, period_hi=300.0, min_period=10, max_period=1000)
     x = tg.generate_host(spec)
     w = (1.0, 0.5, 2.0)
-    p = g.params_for(spec)
-    for c, v in enumerate(w):
-        p.feature_weights[c] = v
-    r = g.detect_rolling(_to_dev(x), p)
-    op = O.params_for(spec, dft_band_only=True, weights=w)
-    agree = 0
-    for i in range(x.shape[0]):
-        o = O.rolling(x[i], op)
-        agree += (r[i]["status"], r[i]["t_init"], r[i]["t_iter"], r[i]["n_sub"]) == (o.status, o.t_init, o.t_iter,
-                                                                                    len(o.sub_start))
-    assert agree >= x.shape[0] - 1
-    m = g.measure_adaptive(_to_dev(x), p, 600)
-    agree = 0
-    for i in range(x.shape[0]):
-        o = O.measure(x[i], op, 600)
-        agree += (int(m[i]["t_iter"]), int(m[i]["rounds"]), int(m[i]["samples"])) == (o["t_iter"], o["rounds"],
-                                                                                       o["samples"])
-    assert agree >= x.shape[0] - 1
+    _rolling_compare(x, spec, "non-pow2-weighted", weights=w)
+    _measure_compare(x, spec, 600, "non-pow2-weighted", weights=w)
+
+
+def test_measure_prefix_lengths_not_multiple_of_4():
+    # ragged Alg. 4 prefixes whose channel stride (the recording length, 3001) is not a
+    # multiple of 4 while some prefix lengths are: the composite must not take the 128-bit
+    # path on misaligned rows
+    spec = tg.CFG2.with_(batch=6, n_samples=3001, period_lo=20.0, period_hi=300.0, min_period=10, max_period=1000)
+    x = tg.generate_host(spec)
+    _measure_compare(x, spec, 600, "n3001")
+
+
+def test_rolling_n_not_multiple_of_4_large_batch():
+    # suffix chunks of a recording whose length is not a multiple of 4, at a batch large
+    # enough that the chunk layout used to outgrow its workspace section
+    spec = tg.CFG2.with_(batch=40, n_samples=2049, period_lo=20.0, period_hi=200.0, min_period=10, max_period=1024)
+    _rolling_compare(tg.generate_host(spec), spec, "n2049-b40")
 
 
 def test_sharded_detect_nccl_world1():
@@ -630,7 +622,7 @@ def test_sharded_detect_nccl_world1():
     spec = tg.CFG2.with_(batch=12)
     x = tg.generate_host(spec)
     p = g.params_for(spec)
-    r1, _, _ = _detect(x, p)
+    r1 = _detect(x, p)[0]
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -643,3 +635,12 @@ def test_sharded_detect_nccl_world1():
         assert out.cpu().numpy().tobytes() == r1.tobytes()
     finally:
         dist.destroy_process_group()
+
+
+def test_measure_empty_band_prefix():
+    # the first prefix's band is empty (L_max clipped to 2500 < L_min = 3000): INSUFFICIENT,
+    # without the band DFT writing past its shared-memory slots
+    spec = tg.CFG2.with_(batch=3, n_samples=20000, period_lo=3200.0, period_hi=4000.0, min_period=3000,
+                         max_period=10000)
+    r = _measure_compare(tg.generate_host(spec), spec, 5000, "empty-band")
+    assert (r["status"] == O.TRACE_INSUFFICIENT).all() and (r["rounds"] == 1).all()

@@ -132,17 +132,22 @@ def _fp32_rounding_is_clear(v64: float, rel=1e-12) -> bool:
     return min(abs(v64 - m) for m in mids) > rel * abs(v64)
 
 
-@pytest.mark.parametrize("F,weights", [(1, None), (3, None), (3, (1.0, 0.5, 2.0)), (2, (0.25, 1.0))])
-def test_composite_is_the_exact_definition_rounded_once(F, weights):
+@pytest.mark.parametrize("F,weights,N", [(1, None, 257), (3, None, 257), (3, (1.0, 0.5, 2.0), 257), (2, (0.25, 1.0), 257),
+                                         (1, None, 65536)])
+def test_composite_is_the_exact_definition_rounded_once(F, weights, N):
     """Z23: y[n] is the exact value of the definition (Z1) sum_c w_c (x_c[n] - mu_c)
     / sigma_c rounded to fp32 once. Reference: a 50-digit decimal evaluation of the
     definition (no binary floating point in it), compared bit for bit wherever the exact
-    value is not within 1e-12 of an fp32 rounding boundary."""
+    value is not within 1e-12 of an fp32 rounding boundary. At N = 2^16 (config 3's length)
+    on integer readings this also checks the statistics' accuracy (a plain running fp64 sum
+    of the squares is up to ~1e-12 off at this length, which moves the rounding of a sample
+    now and then)."""
     from decimal import Decimal, getcontext
     getcontext().prec = 50
     rng = np.random.default_rng(F + (0 if weights is None else 7))
-    N = 257
     x = np.round(rng.uniform(0, 300, (F, N)) + 40 * np.sin(np.arange(N) * 0.07), 1).astype(np.float32)
+    if N > 1000:  # NVML-like integer readings (the GPU composite test's data)
+        x = np.round(rng.uniform(0, 300, (F, N)) + 50 * np.sin(np.arange(N) * 0.01)).astype(np.float32)
     y, _, _, _ = O.composite(x, weights=weights)
     w = [Decimal(float(np.float32(v))) for v in (weights or (1.0,) * F)]
     cols = []
