@@ -122,22 +122,35 @@ def _max_over_ranks(value: float, dev) -> float:
 # ---------------------------------------------------------------------------------------
 # CPU oracle timing (the reference arm and the cpu_baseline object)
 
-def oracle_sample(spec, first: int, count: int, threads: int):
+def oracle_sample(spec, first: int, count: int, threads: int, band_only: bool = False):
     import oracle as O
     import tracegen as tg
     x = tg.generate_host(spec, first, count, threads=threads)
-    p = O.params_for(spec)
+    p = O.params_for(spec, dft_band_only=band_only)
     t0 = time.perf_counter()
     ds = O.detect_batch(x, p, threads=threads)
     dt = time.perf_counter() - t0
     return dt, ds
 
 
-def cpu_baseline(spec, count: int, threads: int) -> dict:
-    dt, ds = oracle_sample(spec, 0, count, threads)
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(spec, count: int, threads: int, name: str = "config 3", band_only: bool = False) -> dict:
+    dt, ds = oracle_sample(spec, 0, count, threads, band_only)
+    dft = ("naive O(N^2) DFT at the bins the peak rule reads (the oracle's dft_band_only mode: the same per-bin "
+           "arithmetic, 1/5 of the bins)" if band_only else "naive O(N^2) DFT over every bin")
     return {"value": count / dt, "unit": "traces/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {count} traces of the workload (config 3 shape), full oracle (naive O(N^2) DFT, "
-                      f"literal Alg. 2 with fp64 CEM), {threads} threads, {dt:.1f} s"}
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "sample": f"first {count} traces of the workload ({name}), the oracle as it stands ({dft}, literal "
+                      f"Alg. 2 with fp64 CEM), {threads} threads, {dt:.1f} s"}
 
 
 def run_reference(args) -> None:
@@ -163,6 +176,7 @@ def run_reference(args) -> None:
         "config": {"workload": "cfg3 shape: traces x 3 features x 2^16 samples (sample of "
                                f"{per_step} traces per step)", "traces_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "traces/s", "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count(),
                          "sample": f"{per_step} traces per step x {args.steps} steps on {threads} host threads"},
         "e2e": {"value": value, "unit": "traces/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -178,41 +192,85 @@ def run_gpu(args) -> None:
 
     import paper_2201_01684_b200 as g
     import tracegen as tg
+    from paper_2201_01684_b200 import shard
 
     world, rank, local = _dist()
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    spec = tg.CFG3.with_(batch=args.batch)
-    B = args.batch
-    p = g.params_for(spec)
     stream = torch.cuda.current_stream()
+    # the workload: config 3 (10^5 traces resident on one GPU) at N = 1; config 4 (10^6 traces
+    # sharded over the N GPUs, each shard streamed through a resident buffer of at most
+    # --max-chunk traces when it exceeds HBM) at N > 1 (or --cfg4)
+    cfg4 = world > 1 or args.cfg4
+    if cfg4:
+        spec = tg.CFG4.with_(batch=args.cfg4_total)
+        first, B = shard.shard_range(spec.batch, world, rank)
+    else:
+        spec = tg.CFG3.with_(batch=args.batch)
+        first, B = 0, args.batch
+    chunks = shard.chunk_ranges(first, B, args.max_chunk)
+    streamed = len(chunks) > 1
+    Bbuf = max(n for _, n in chunks) if chunks else 1
+    p = g.params_for(spec)
 
-    # inputs resident in HBM before timing: this rank's shard of the global index space
-    x = torch.empty((B, spec.n_features * spec.n_samples), dtype=torch.float32, device=dev)
-    tg.generate_device(spec, x, first=rank * B, count=B, stream=stream.cuda_stream)
-    ws = g.alloc_workspace(g.workspace_size(p, B), dev)
-    res = torch.empty(B * g.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-    gathered = torch.empty(world * B * g.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev) if world > 1 else None
+    # inputs resident in HBM before timing (this rank's shard, or its first chunk), generated
+    # on the device from (seed, global index)
+    x = torch.empty((Bbuf, spec.n_features * spec.n_samples), dtype=torch.float32, device=dev)
+    tg.generate_device(spec, x, first=first, count=min(B, Bbuf), stream=stream.cuda_stream)
+    ws = g.alloc_workspace(g.workspace_size(p, Bbuf), dev)
+    res = torch.empty(max(B, 1) * g.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
-    def step(evs=None):
-        if evs is None:
-            g.detect_periods(x, p, workspace=ws, results=res, stream=stream)
-        else:
-            g.detect_periods_timed(x, p, ws, res, evs, stream=stream)
+    def gather():
         if world > 1:
             if BACKEND == "nccl":
-                dist.all_gather_into_tensor(gathered, res)  # the only device-to-device transfer
-            else:
-                g_cpu = torch.empty(gathered.shape, dtype=gathered.dtype)
-                dist.all_gather_into_tensor(g_cpu, res.cpu())
-                gathered.copy_(g_cpu)
+                return shard.gather_results(res[:B * g.RESULT_DTYPE.itemsize], spec.batch)  # the only device-to-device transfer
+            out = shard.gather_results(res[:B * g.RESULT_DTYPE.itemsize].cpu(), spec.batch)
+            return out.to(dev)
+        return None
 
-    for _ in range(args.warmup):
-        step()
+    def step(evs=None):
+        # resident shard: one call over all of it
+        if evs is None:
+            g.detect_periods(x[:B], p, workspace=ws, results=res, stream=stream)
+        else:
+            g.detect_periods_timed(x[:B], p, ws, res, evs, stream=stream)
+        gather()
+
+    chunk_ms = []
+
+    def step_streamed():
+        # streamed shard (config 4 at N = 2, 4): chunk i's traces are generated into the
+        # resident buffer (untimed), then its detect call is timed with CUDA events; the
+        # step's time is the sum over chunks plus the all-gather
+        ms = 0.0
+        for i, (f, n) in enumerate(chunks):
+            tg.generate_device(spec, x[:n], first=f, count=n, stream=stream.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            off = (f - first) * g.RESULT_DTYPE.itemsize
+            g.detect_periods(x[:n], p, workspace=ws, results=res[off:off + n * g.RESULT_DTYPE.itemsize], stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gather()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+        chunk_ms.append(ms)
+
+    if streamed:
+        for _ in range(args.warmup):
+            step_streamed()
+        chunk_ms.clear()
+    else:
+        for _ in range(args.warmup):
+            step()
     torch.cuda.synchronize()
-    counters = g.read_counters(ws, p, B)
+    counters = g.read_counters(ws, p, Bbuf)
 
     # phase events per timed step (live per-kernel timing on the launching stream)
     phase_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
@@ -226,19 +284,40 @@ def run_gpu(args) -> None:
     torch.cuda.synchronize()
     sampler.start()
     time.sleep(0.3)
-    t_start.record(stream)
-    for k in range(args.steps):
-        step(phase_evs[k])
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    if streamed:
+        for k in range(args.steps):
+            step_streamed()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        elapsed_ms = _max_over_ranks(sum(chunk_ms), dev)
+    else:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(phase_evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        elapsed_ms = _max_over_ranks(t_start.elapsed_time(t_end), dev)
     clocks = sampler.stop()
-    elapsed_ms = _max_over_ranks(t_start.elapsed_time(t_end), dev)
-    phases = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)] for evs in phase_evs])  # ms
+    if streamed:
+        # phase split of one chunk call (timed separately after the run, resident chunk)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        for e in evs:
+            e.record(stream)
+        g.detect_periods_timed(x[:chunks[-1][1]], p, ws, res, evs, stream=stream)
+        torch.cuda.synchronize()
+        phases = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)]])
+        counters = g.read_counters(ws, p, chunks[-1][1])
+        ph_traces = chunks[-1][1]
+    else:
+        phases = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)] for evs in phase_evs])  # ms
+        ph_traces = B
     phase_ms = phases.mean(axis=0)
 
-    value = world * B * args.steps / (elapsed_ms / 1e3)
+    total_traces = spec.batch if cfg4 else world * B
+    value = total_traces * args.steps / (elapsed_ms / 1e3)
     peaks, peak_kind = _peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
 
@@ -249,36 +328,44 @@ def run_gpu(args) -> None:
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tj = json.load(f)
-        traffic = tj["scorer_dram_bytes_per_trace"] * B
+        traffic = tj["scorer_dram_bytes_per_trace"] * ph_traces
         traffic_note = tj.get("note")
         traffic_spec = tj["spectral_only_dram_bytes_per_trace"] * B
     except Exception:
         pass
     # dominant kernel: the Alg. 2 scorer (two launches per step, candidate + local queries)
     score_ms = phase_ms[2] + phase_ms[4]
-    passes = counters["cem_sample_passes"]  # per step (samples x CEM passes, incl. the W_{i+1} pass)
+    passes = counters["cem_sample_passes"]  # per call (samples x CEM passes, incl. the W_{i+1} pass)
     dp_per_pass = 3 * p.num_groups + 2
     achieved_dp = passes * dp_per_pass / (score_ms / 1e3)  # fp64 instr/s
     peak_dp = SM_COUNT * DP_PER_CLK_PER_SM * sm_max * 1e6
     hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
-    alg_bytes = B * (4 * spec.n_features * spec.n_samples + 24)
+    alg_bytes = ph_traces * (4 * spec.n_features * spec.n_samples + 24)
     spec_ms = phase_ms[0] + phase_ms[1]
+    if cfg4:
+        workload = (f"cfg4: 1e6 traces x 3 features x 2^16 samples sharded over {world} GPU(s) (BASELINE.json config 4), "
+                    f"{B} traces per rank" + (f", streamed in {len(chunks)} chunks of <= {args.max_chunk}" if streamed
+                                              else ", resident"))
+    else:
+        workload = "cfg3: 1e5 traces x 3 features x 2^16 samples on 1 GPU (BASELINE.json config 3)"
     line = {
         "metric": METRIC, "value": value, "unit": "traces/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3: 1e5 traces x 3 features x 2^16 samples per GPU (BASELINE.json config 3; "
-                               "configs 4 = the same shards at N>1)", "batch_per_gpu": B,
+        "scaling": "strong" if cfg4 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "batch_per_gpu": B, "traces_total": total_traces,
                    "n_samples": spec.n_samples, "n_features": spec.n_features,
                    "period_bounds": [spec.min_period, spec.max_period], "num_groups": p.num_groups,
                    "max_candidates": p.max_candidates, "c_peak": round(p.c_peak, 4),
-                   "l2": "inputs larger than L2 (%.1f GB/GPU vs 126 MB)" % (B * 4 * 3 * spec.n_samples / 1e9),
+                   "l2": "inputs larger than L2 (%.1f GB/GPU vs 126 MB)" % (Bbuf * 4 * 3 * spec.n_samples / 1e9),
+                   "timing": ("sum of per-chunk CUDA-event times of the detect calls + all-gather; chunk generation "
+                              "between them excluded" if streamed else "CUDA events around K whole steps"),
                    "parallelism": f"dp{world} (trace shards, NCCL all-gather of results)"},
-        "hbm_frac_end_to_end": (alg_bytes / (elapsed_ms / args.steps / 1e3) / 1e9) / hbm_peak,
+        "hbm_frac_end_to_end": (total_traces / world * (4 * spec.n_features * spec.n_samples + 24)
+                                / (elapsed_ms / args.steps / 1e3) / 1e9) / hbm_peak,
         "roofline": {"bound": "alu", "kernel": "score_kernel (Alg. 2 CEM scorer, 2 launches/step)",
                      "achieved": achieved_dp / 1e12, "peak": peak_dp / 1e12, "unit": "TDPinstr/s",
                      "frac": achieved_dp / peak_dp, "traffic": traffic, "traffic_note": traffic_note,
-                     "work": f"{passes} CEM sample-passes/step x {dp_per_pass} fp64 instr",
+                     "work": f"{passes} CEM sample-passes/call x {dp_per_pass} fp64 instr",
                      "peak_note": f"148 SMs x 64 fp64/clk x {sm_max:.0f} MHz (sm_max_mhz, {peak_kind})"},
         "roofline_spectral": {"bound": "hbm", "kernel": "composite + spectrum (a1-a3)",
                               "achieved": alg_bytes / (spec_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -287,9 +374,10 @@ def run_gpu(args) -> None:
         "phase_ms": {n: float(v) for n, v in zip(g.PHASES, phase_ms)},
         "work_counters": counters,
         "clocks": clocks,
-        # fused spectrum (1), 2 x scorer (team, mid and xl bucketed: 3), select (1), final (1)
-        "gpu_launches": 9 * args.steps,
+        # fused spectrum (1), 2 x scorer (team, mid and xl bucketed: 3), select (1), final (1) per call
+        "gpu_launches": 9 * args.steps * len(chunks),
     }
+    B = min(B, Bbuf)  # the sub-lines below use the resident buffer
 
     # spectral-only detector (rows a1-a3 + arg-max, T_iter = 1/f_major) on
     # the same resident traces: the HBM-bound path, 4*F*N bytes read per trace, 16 B written
@@ -404,17 +492,76 @@ def run_gpu(args) -> None:
             "mean_probes_sm": float(gr["probes_sm"].mean()), "mean_probes_mem": float(gr["probes_mem"].mean()),
             "gears": f"{len(smg)} SM x {len(memg)} memory", "note": "control logic, one thread per workload"}
 
-    # e2e: same metric through the public host entry point (pinned host buffers, H2D+D2H inside)
-    del x
+    del x, ws
     torch.cuda.empty_cache()
+
+    # BASELINE config 5 (the hard case: 10^4 traces x 3 x 2^18, mid-trace period shift,
+    # harmonic-aliased spectra): the whole Alg. 1 path, inputs resident, its own rooflines
+    # (spectral stage vs HBM, scorer vs fp64) and an oracle subset on the host cores
+    if world == 1 and not args.no_cfg5:
+        spec5 = tg.CFG5.with_(batch=args.cfg5_batch)
+        B5 = spec5.batch
+        p5 = g.params_for(spec5)
+        x5 = torch.empty((B5, spec5.n_features * spec5.n_samples), dtype=torch.float32, device=dev)
+        tg.generate_device(spec5, x5, stream=stream.cuda_stream)
+        ws5 = g.alloc_workspace(g.workspace_size(p5, B5), dev)
+        res5 = torch.empty(B5 * g.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        for _ in range(args.warmup):
+            g.detect_periods(x5, p5, workspace=ws5, results=res5, stream=stream)
+        torch.cuda.synchronize()
+        c5 = g.read_counters(ws5, p5, B5)
+        evs5 = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+        for evs in evs5:
+            for e in evs:
+                e.record(stream)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a0.record(stream)
+        for k in range(args.steps):
+            g.detect_periods_timed(x5, p5, ws5, res5, evs5[k], stream=stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ms5 = a0.elapsed_time(a1) / args.steps
+        ph5 = np.array([[evs[i].elapsed_time(evs[i + 1]) for i in range(6)] for evs in evs5]).mean(axis=0)
+        r5 = g.results_numpy(res5)
+        bytes5 = B5 * (4 * spec5.n_features * spec5.n_samples + 24)
+        sp5 = ph5[0] + ph5[1]
+        sc5 = ph5[2] + ph5[4]
+        dp5 = c5["cem_sample_passes"] * (3 * p5.num_groups + 2) / (sc5 / 1e3)
+        line["cfg5"] = {
+            "metric": "traces/sec period-detected (2^18 samples x 3 features, BASELINE config 5)",
+            "value": B5 / (ms5 / 1e3), "unit": "traces/s", "ms_per_step": ms5, "steps": args.steps,
+            "config": {"workload": "cfg5: 1e4 traces x 3 features x 2^18 samples, mid-trace period shift "
+                                   "(L2 = L1 x U(1.2, 1.6)), harmonic-aliased profiles, interference above Nyquist",
+                       "batch": B5, "period_bounds": [spec5.min_period, spec5.max_period],
+                       "l2": "inputs larger than L2 (%.1f GB vs 126 MB)" % (B5 * 12 * spec5.n_samples / 1e9)},
+            "phase_ms": {n: float(v) for n, v in zip(g.PHASES, ph5)},
+            "roofline_spectral": {"bound": "hbm", "kernel": "composite_kernel + spectrum_kernel<14, 8> (8-CTA cluster FFT)",
+                                  "achieved": bytes5 / (sp5 / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                  "frac": bytes5 / (sp5 / 1e3) / 1e9 / hbm_peak, "peak_kind": peak_kind},
+            "roofline": {"bound": "alu", "kernel": "score kernels (Alg. 2 CEM scorer)", "achieved": dp5 / 1e12,
+                         "peak": peak_dp / 1e12, "unit": "TDPinstr/s", "frac": dp5 / peak_dp,
+                         "work": f"{c5['cem_sample_passes']} CEM sample-passes/step x {3 * p5.num_groups + 2} fp64 instr"},
+            "work_counters": c5,
+            "status_counts": {str(k): int(v) for k, v in zip(*np.unique(r5["status"], return_counts=True))},
+            "gpu_launches": 10 * args.steps,  # composite, cluster spectrum, 2 x 3 scorers, select, final
+        }
+        if rank == 0 and not args.no_cpu_baseline:
+            line["cfg5"]["cpu_baseline"] = cpu_baseline(spec5, args.cfg5_cpu_traces, os.cpu_count() or 1,
+                                                        "config 5", band_only=True)
+        del x5, ws5, res5
+        torch.cuda.empty_cache()
+
+    # e2e: same metric through the public host entry point (pinned host buffers, H2D+D2H inside)
     if not args.no_e2e:
-        # pinned host memory is shared by the ranks of the box: 8192 traces (6.4 GB) per rank at N > 1
-        Be = min(args.e2e_batch, B) if world == 1 else min(args.e2e_batch, B, 8192)
+        # pinned host memory is shared by the ranks of the box: the whole batch at N = 1 (78.6 GB
+        # of the box's 196 GB), 8192 traces (6.4 GB) per rank at N > 1
+        Be = (min(args.e2e_batch, B) if args.e2e_batch else B) if world == 1 else min(args.e2e_batch or B, B, 8192)
         xh = torch.empty((Be, spec.n_features * spec.n_samples), dtype=torch.float32, pin_memory=True)
         tmp = torch.empty((min(Be, 4096), spec.n_features * spec.n_samples), dtype=torch.float32, device=dev)
         for i0 in range(0, Be, tmp.shape[0]):
             n = min(tmp.shape[0], Be - i0)
-            tg.generate_device(spec, tmp, first=rank * B + i0, count=n, stream=stream.cuda_stream)
+            tg.generate_device(spec, tmp, first=first + i0, count=n, stream=stream.cuda_stream)
             xh[i0:i0 + n].copy_(tmp[:n])
         del tmp
         torch.cuda.synchronize()
@@ -459,10 +606,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=100_000)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-batch", type=int, default=16384)
+    ap.add_argument("--e2e-batch", type=int, default=0, help="0: the whole batch at N = 1")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--chunk", type=int, default=2048)
-    ap.add_argument("--cpu-traces", type=int, default=48)
+    ap.add_argument("--cpu-traces", type=int, default=256)
+    ap.add_argument("--cfg4", action="store_true", help="config 4 sharding at N = 1 too (streamed chunks)")
+    ap.add_argument("--cfg4-total", type=int, default=1_000_000)
+    ap.add_argument("--max-chunk", type=int, default=125_000, help="traces resident per GPU (HBM bound)")
+    ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--cfg5-batch", type=int, default=10_000)
+    ap.add_argument("--cfg5-cpu-traces", type=int, default=16)
     ap.add_argument("--ref-traces", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

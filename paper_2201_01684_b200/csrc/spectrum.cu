@@ -724,6 +724,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
   }
   const float2 w32768 = make_float2(9.999999816164e-01f, -1.917475973107e-04f);
   if (cid < p.batch) prefetch_half<F>(x + (int64_t)cid * p.stride, q);
+  // the partner CTA must have started before its shared memory is written (phase A's stats
+  // exchange of the first trace): one cluster barrier per launch (racecheck: "block that
+  // might not have entered yet")
+  cluster.sync();
   for (int64_t t = cid; t < p.batch; t += nclusters) {
     const float* xt = x + t * p.stride;
     // ---- A: stats over my quarter blocks {q, 2 + q} -----------------------------------

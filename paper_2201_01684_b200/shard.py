@@ -40,6 +40,47 @@ def gather_results(local, total: int, group=None):
     return out[: total * RESULT_BYTES]
 
 
+def chunk_ranges(first: int, count: int, max_chunk: int) -> list[tuple[int, int]]:
+    """Split a shard [first, first + count) into consecutive chunks of at most max_chunk
+    traces (config 4 at W = 2 and 4: a shard of 10^6/W traces exceeds one B200's HBM, so it is
+    streamed through a resident buffer chunk by chunk)."""
+    if max_chunk < 1:
+        raise ValueError("max_chunk must be >= 1")
+    out, pos, end = [], first, first + count
+    while pos < end:
+        n = min(max_chunk, end - pos)
+        out.append((pos, n))
+        pos += n
+    return out
+
+
+def detect_shard_chunked(fill, first: int, count: int, max_chunk: int, params, x_buf, results, workspace=None,
+                         stream=None, on_chunk=None, detect=None):
+    """Alg. 1 over this rank's shard in chunks through one resident input buffer.
+
+    fill(x_view, first, n) writes the traces [first, first + n) into x_view (device
+    generation, or a host copy); x_buf is a CUDA tensor [>= max_chunk][stride]; results is a
+    uint8 CUDA tensor [count * 24] receiving the shard's records in global order. on_chunk(i,
+    first, n, phase) is called with phase "filled" after fill and "done" after the detect call
+    was enqueued (the bench times the detect calls alone with CUDA events there). detect
+    defaults to gpoeo_detect_periods (the CPU tests pass a stand-in). Returns the workspace
+    (reused across chunks)."""
+    if detect is None:
+        from . import detect_periods as detect
+
+    for i, (f, n) in enumerate(chunk_ranges(first, count, max_chunk)):
+        xv = x_buf[:n]
+        fill(xv, f, n)
+        if on_chunk:
+            on_chunk(i, f, n, "filled")
+        off = (f - first) * RESULT_BYTES
+        _, _, workspace = detect(xv, params, workspace=workspace, results=results[off:off + n * RESULT_BYTES],
+                                 stream=stream)
+        if on_chunk:
+            on_chunk(i, f, n, "done")
+    return workspace
+
+
 def detect_sharded(x_local, total: int, params, workspace=None, stream=None, group=None):
     """Run gpoeo_detect_periods on this rank's shard (CUDA tensor [count][stride]) and
     all-gather the results of all ranks (returns a uint8 tensor [total * 24])."""

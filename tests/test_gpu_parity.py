@@ -633,6 +633,15 @@ def test_sharded_detect_nccl_world1():
         out, _ = shard.detect_sharded(_to_dev(x), spec.batch, p)
         torch.cuda.synchronize()
         assert out.cpu().numpy().tobytes() == r1.tobytes()
+        # config 4's streamed shard: the same traces through a 5-trace resident buffer in
+        # chunks (generated on the device per chunk), then the all-gather
+        xb = torch.empty((5, spec.n_features * spec.n_samples), dtype=torch.float32, device="cuda")
+        res = torch.empty(spec.batch * shard.RESULT_BYTES, dtype=torch.uint8, device="cuda")
+        shard.detect_shard_chunked(lambda xv, f, n: tg.generate_device(spec, xv, first=f, count=n), 0, spec.batch,
+                                   5, p, xb, res)
+        out2 = shard.gather_results(res, spec.batch)
+        torch.cuda.synchronize()
+        assert out2.cpu().numpy().tobytes() == r1.tobytes()
     finally:
         dist.destroy_process_group()
 

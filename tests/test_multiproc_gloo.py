@@ -78,3 +78,58 @@ def test_shard_ranges_partition():
                     assert f == pos
                     pos += c
             assert max(c for _, c in spans) <= shard.padded_shard(total, world) or total == 0
+
+
+def _chunked_worker(rank, world, port, total, max_chunk, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    first, count = shard.shard_range(total, world, rank)
+    x_buf = torch.zeros((max(1, min(max_chunk, count)), 1), dtype=torch.int64)  # trace index per row
+    results = torch.zeros(count * shard.RESULT_BYTES, dtype=torch.uint8)
+    seen = []
+
+    def fill(xv, f, n):
+        xv[:, 0] = torch.arange(f, f + n)
+
+    def fake_detect(xv, params, workspace=None, results=None, stream=None):
+        idx = xv[:, 0].numpy()
+        results.copy_(torch.from_numpy(_fake_results(int(idx[0]), len(idx)).view(np.uint8).copy()))
+        return results, None, workspace
+
+    shard.detect_shard_chunked(fill, first, count, max_chunk, None, x_buf, results,
+                               on_chunk=lambda i, f, n, ph: seen.append((i, f, n, ph)), detect=fake_detect)
+    out = shard.gather_results(results, total)
+    q.put((rank, first, count, seen, out.numpy().tobytes()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total,max_chunk", [(10, 3), (1000, 125), (7, 100), (9, 1)])
+def test_chunked_shards_match_world1(total, max_chunk):
+    """Config 4's streamed shards (row e): each rank runs its shard through one resident
+    buffer in chunks of <= max_chunk traces; the all-gathered records equal the W = 1 ones."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunked_worker, args=(r, world, port, total, max_chunk, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = _fake_results(0, total).view(np.uint8).tobytes()
+    for _, first, count, seen, blob in got:
+        assert blob == want
+        chunks = [(f, n) for i, f, n, ph in seen if ph == "done"]
+        assert chunks == shard.chunk_ranges(first, count, max_chunk)
+        assert all(n <= max_chunk for _, n in chunks) and sum(n for _, n in chunks) == count
+
+
+def test_chunk_ranges():
+    assert shard.chunk_ranges(0, 10, 4) == [(0, 4), (4, 4), (8, 2)]
+    assert shard.chunk_ranges(500_000, 500_000, 125_000) == [(500_000 + i * 125_000, 125_000) for i in range(4)]
+    assert shard.chunk_ranges(5, 0, 3) == []
+    with pytest.raises(ValueError):
+        shard.chunk_ranges(0, 1, 0)
