@@ -83,12 +83,13 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    try:
-        _build.build()
-    except Exception as e:  # nvcc missing on a run box: use the shipped .so if present
-        if not os.path.exists(path):
-            raise GpoeoError(f"libgpoeo.so is missing and cannot be built: {e}") from e
+    path = os.environ.get("GPOEO_LIB") or _build.LIB  # GPOEO_LIB: a prebuilt variant (profiling experiments)
+    if not os.environ.get("GPOEO_LIB"):
+        try:
+            _build.build()
+        except Exception as e:  # nvcc missing on a run box: use the shipped .so if present
+            if not os.path.exists(path):
+                raise GpoeoError(f"libgpoeo.so is missing and cannot be built: {e}") from e
     lib = ctypes.CDLL(path)
     P = ctypes.c_void_p
     PP = ctypes.POINTER(GpoeoParams)

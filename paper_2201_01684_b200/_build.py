@@ -28,14 +28,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None) -> str:
+    """Build libgpoeo.so (or, with out/extra, a variant with extra nvcc flags at `out`: the
+    profiling experiments' builds, loaded through GPOEO_LIB)."""
+    if out is None and not force and not _stale():
         return LIB
+    lib = out or LIB
+    flags = NVCC_FLAGS + (extra or [])
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = lib + "." + src.replace(".cu", ".o")
+        cmd = ["nvcc", *flags, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
@@ -47,13 +51,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed")
         if verbose and out:
             sys.stderr.write(out)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python _build.py [--force] [-v] [--out PATH -- extra nvcc flags...]
+    argv = sys.argv[1:]
+    extra = argv[argv.index("--") + 1:] if "--" in argv else []
+    out = argv[argv.index("--out") + 1] if "--out" in argv else None
+    print(build(force="--force" in argv, verbose="-v" in argv, out=out, extra=extra))
