@@ -247,10 +247,10 @@ void gpoeo_default_rolling_params(gpoeo_rolling_params* rp);
 size_t gpoeo_workspace_size_rolling(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t batch);
 
 /* Alg. 3 over a batch of recorded traces (device pointers as gpoeo_detect_periods; results
- * [batch] device). The suffixes of all traces run through Alg. 1 as ragged batches of up to
- * `batch` rows (each row a one-channel sequence of its own length); the suffix plan needs
- * T_init on the host, so this entry point SYNCHRONISES `stream` (once in the middle and
- * before returning). */
+ * [batch] device). Alg. 1 runs on the whole traces; the suffix plan (lines 2-13) is computed
+ * from T_init on the device; the suffixes run through Alg. 1 as ragged batches (batch j = the
+ * j-th suffix of every trace, each row a one-channel sequence of its own length). Asynchronous,
+ * allocation-free, no host round trip (like gpoeo_detect_periods). */
 int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
                          gpoeo_rolling_result* results, void* workspace, size_t workspace_bytes, void* stream);
 
@@ -280,8 +280,8 @@ size_t gpoeo_workspace_size_measure(const gpoeo_params* p, const gpoeo_rolling_p
 
 /* Alg. 4 over `batch` sessions. traces: device [batch][trace_stride], the recordings
  * (n_samples = the recording length); init_samples: SmpDur_init / T_s + 1, in [8, n_samples];
- * results: HOST [batch]. SYNCHRONISES `stream` (every round needs the previous one's
- * SmpDur_next on the host). */
+ * results: HOST [batch]. SYNCHRONISES `stream` once per round (each round's Alg. 3 runs on the
+ * device; its SmpDur_next values are read back to decide which sessions wait for more samples). */
 int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
                            int32_t init_samples, gpoeo_measure_result* results, void* workspace,
                            size_t workspace_bytes, void* stream);

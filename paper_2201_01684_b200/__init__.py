@@ -339,9 +339,11 @@ def default_rolling_params(**kw) -> GpoeoRollingParams:
     return rp
 
 
-def detect_rolling(traces, p: GpoeoParams, rp: GpoeoRollingParams | None = None, stream=None) -> np.ndarray:
+def detect_rolling_async(traces, p: GpoeoParams, rp: GpoeoRollingParams | None = None, workspace=None, results=None,
+                         stream=None):
     """Alg. 3 (reading R5) on a CUDA float32 tensor of recorded traces
-    [B][trace_stride]; synchronous; returns ROLLING_DTYPE records on the host."""
+    [B][trace_stride]: enqueued on `stream`, no host round trip. Returns (results uint8 device
+    tensor of ROLLING_DTYPE records, workspace)."""
     import torch
     assert traces.is_cuda and traces.dtype == torch.float32 and traces.is_contiguous()
     B = traces.shape[0]
@@ -351,12 +353,23 @@ def detect_rolling(traces, p: GpoeoParams, rp: GpoeoRollingParams | None = None,
     if need == 0:
         _check(validate(p), "params")
         raise GpoeoError("invalid rolling parameters")
-    ws = alloc_workspace(need, traces.device)
-    out = torch.empty(B * ROLLING_DTYPE.itemsize, dtype=torch.uint8, device=traces.device)
+    if workspace is None or workspace.numel() < need:
+        workspace = alloc_workspace(need, traces.device)
+    if results is None:
+        results = torch.empty(B * ROLLING_DTYPE.itemsize, dtype=torch.uint8, device=traces.device)
     rc = lib.gpoeo_detect_rolling(ctypes.c_void_p(traces.data_ptr()), B, ctypes.byref(p), ctypes.byref(rp),
-                                  ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
-                                  _stream_handle(stream))
+                                  ctypes.c_void_p(results.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+                                  workspace.numel(), _stream_handle(stream))
     _check(rc, "gpoeo_detect_rolling")
+    return results, workspace
+
+
+def detect_rolling(traces, p: GpoeoParams, rp: GpoeoRollingParams | None = None, stream=None) -> np.ndarray:
+    """detect_rolling_async, then the records on the host (ROLLING_DTYPE)."""
+    import torch
+    out, _ = detect_rolling_async(traces, p, rp, stream=stream)
+    if stream is not None and not isinstance(stream, int):
+        torch.cuda.current_stream().wait_stream(stream)
     return out.cpu().numpy().view(ROLLING_DTYPE)
 
 

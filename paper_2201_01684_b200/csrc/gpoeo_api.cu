@@ -254,7 +254,7 @@ static gpoeo_params suffix_params(const gpoeo_params* p, int32_t Nj) {
 }
 
 struct RollLayout {
-  size_t main, whole, plan, segs, gtrace, gstart, gseg, grown, gsig, gres, gdet, gws, total;
+  size_t main, whole, plan, segs, gstart, glen, gsig, gres, gdet, gws, total;
   int64_t max_sub;
 };
 
@@ -264,6 +264,16 @@ static Plan main_plan(const gpoeo_params* p, int64_t B, bool ragged) {
   Plan pm = make_plan(p, B);
   if (ragged) pm.max_local = (int64_t)pm.Lmax - pm.Lmin + 1;
   return pm;
+}
+
+// Alg. 1 plan of one suffix batch: B rows of at most N samples (row length N rounded up to a
+// multiple of 4 floats); local ranges bounded by the band (rows clip L_max to N_j/2)
+static Plan suffix_plan(const gpoeo_params* p, int64_t B, gpoeo_params* q_out) {
+  const gpoeo_params q = suffix_params(p, (p->n_samples + 3) & ~3);
+  Plan pl = make_plan(&q, B);
+  pl.max_local = q.max_period >= q.min_period ? (int64_t)q.max_period - q.min_period + 1 : 0;
+  if (q_out) *q_out = q;
+  return pl;
 }
 
 static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_params* rp, int64_t B,
@@ -280,31 +290,27 @@ static RollLayout rolling_layout(const gpoeo_params* p, const gpoeo_rolling_para
   R.whole = take(sizeof(gpoeo_result) * (size_t)B);
   R.plan = take(sizeof(RollTrace) * (size_t)B);
   R.segs = take(sizeof(RollSeg) * (size_t)B * (size_t)R.max_sub);
-  R.gtrace = take(sizeof(int32_t) * (size_t)B);
-  R.gstart = take(sizeof(int32_t) * (size_t)B);
-  R.gseg = take(sizeof(int32_t) * (size_t)B);
-  R.grown = take(sizeof(int32_t) * (size_t)B);
+  R.gstart = take(sizeof(int32_t) * (size_t)B * (size_t)R.max_sub);  // [max_sub][B]
+  R.glen = take(sizeof(int32_t) * (size_t)B * (size_t)R.max_sub);
   R.gsig = take(sizeof(float) * (size_t)B * (size_t)((p->n_samples + 3) & ~3));
   R.gres = take(sizeof(gpoeo_result) * (size_t)B);
   R.gdet = take(sizeof(gpoeo_detail) * (size_t)B);
-  // one chunk of suffixes: at most B rows of at most N samples (rows padded to a multiple of 4
-  // floats, so the chunk's row length may reach N rounded up); local ranges bounded by the band
-  gpoeo_params q = suffix_params(p, (p->n_samples + 3) & ~3);
-  Plan pl = make_plan(&q, B);
-  pl.max_local = (int64_t)q.max_period - q.min_period + 1;
-  R.gws = take(layout(pl).total);
+  R.gws = take(layout(suffix_plan(p, B, nullptr)).total);
   R.total = o;
   return R;
 }
 
-// Alg. 3 on `batch` traces (whole traces, or with host_len: row t = the first host_len[t]
-// samples of trace dev_idx[t], dev_len a device copy of host_len); R laid out for it.
+// Alg. 3 on `batch` traces (whole traces, or with dev_len: row t = the first dev_len[t]
+// samples of trace dev_idx[t]); R laid out for it. Device-side throughout: Alg. 1 on the whole
+// traces, the suffix plan from T_init (rolling_plan_kernel, lines 2-13), then max_sub ragged
+// Alg. 1 batches -- batch j holds the j-th suffix of every trace (a row without one has
+// length 0 and finds no period) -- and lines 14-21. Asynchronous, no host round trip.
 static int rolling_core(const float* traces, int64_t batch, const gpoeo_params* p, const gpoeo_rolling_params* rp,
-                        const int32_t* host_len, const int32_t* dev_len, const int32_t* dev_idx,
-                        gpoeo_rolling_result* results, char* b, const RollLayout& R, cudaStream_t s) {
+                        const int32_t* dev_len, const int32_t* dev_idx, gpoeo_rolling_result* results, char* b,
+                        const RollLayout& R, cudaStream_t s) {
   // line 1: T_init = Alg. 1 on every whole trace (the composite y stays in the workspace)
-  Plan pm = main_plan(p, batch, host_len != nullptr);
-  if (host_len) {  // ragged whole traces: row t = trace idx[t], its first len[t] samples of every channel
+  Plan pm = main_plan(p, batch, dev_len != nullptr);
+  if (dev_len) {  // ragged whole traces: row t = trace idx[t], its first len[t] samples of every channel
     pm.row_n = dev_len;
     pm.row_idx = dev_idx;
   }
@@ -313,98 +319,32 @@ static int rolling_core(const float* traces, int64_t batch, const gpoeo_params* 
   int rc = run_detect(traces, pm, Lm, b + R.main, whole, nullptr, s);
   if (rc != GPOEO_OK) return rc;
   const float* y = carve(pm, Lm, b + R.main).y;
-  std::vector<gpoeo_result> hw((size_t)batch);
-  CK(cudaMemcpyAsync(hw.data(), whole, sizeof(gpoeo_result) * (size_t)batch, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  // lines 2-13 on the host (exact sample arithmetic, as the oracle): the suffix plan
   const int32_t N = p->n_samples;  // row stride of y
-  std::vector<RollTrace> plan((size_t)batch);
-  std::vector<int32_t> sfx_trace, sfx_start;
-  for (int64_t t = 0; t < batch; ++t) {
-    RollTrace& pt = plan[(size_t)t];
-    pt.first = (int32_t)sfx_trace.size();
-    pt.n_sub = 0;
-    pt.early = 0;
-    pt.pad = 0;
-    if (hw[(size_t)t].status != GPOEO_TRACE_OK) continue;
-    const int32_t Nt = host_len ? host_len[t] : N;
-    const double smpdur = (double)(Nt - 1);
-    const double L0 = (double)hw[(size_t)t].period;
-    if (smpdur < rp->c_measure * L0) {
-      pt.early = 1;
-      continue;
-    }
-    double ts = smpdur - (2.0 + rp->c_eval * rp->step) * L0;
-    if (ts < 0.0) ts = 0.0;
-    while ((smpdur - ts) / L0 >= rp->c_measure && pt.n_sub < R.max_sub) {
-      const int32_t s0 = (int32_t)floor(ts);
-      sfx_trace.push_back((int32_t)t);
-      sfx_start.push_back(s0);
-      ++pt.n_sub;
-      ts += rp->step * L0;
-    }
-  }
+  RollParamsDev rpd{rp->c_measure, rp->step, rp->c_eval, rp->diff_threshold};
   RollTrace* dplan = reinterpret_cast<RollTrace*>(b + R.plan);
   RollSeg* dsegs = reinterpret_cast<RollSeg*>(b + R.segs);
-  CK(cudaMemcpyAsync(dplan, plan.data(), sizeof(RollTrace) * (size_t)batch, cudaMemcpyHostToDevice, s));
-  if (!sfx_trace.empty())
-    CK(cudaMemsetAsync(dsegs, 0xFF, sizeof(RollSeg) * sfx_trace.size(), s));  // period -1: none
-  // Alg. 1 on every suffix (line 11): the suffixes, each a one-channel sequence of its own
-  // length, run as ragged batches of up to `batch` rows (per-row N: Plan::row_n)
-  int32_t* gtrace = reinterpret_cast<int32_t*>(b + R.gtrace);
   int32_t* gstart = reinterpret_cast<int32_t*>(b + R.gstart);
-  int32_t* gseg = reinterpret_cast<int32_t*>(b + R.gseg);
-  int32_t* grown = reinterpret_cast<int32_t*>(b + R.grown);
+  int32_t* glen = reinterpret_cast<int32_t*>(b + R.glen);
   float* gsig = reinterpret_cast<float*>(b + R.gsig);
   gpoeo_result* gres = reinterpret_cast<gpoeo_result*>(b + R.gres);
   gpoeo_detail* gdet = reinterpret_cast<gpoeo_detail*>(b + R.gdet);
-  // suffixes shorter than the smallest supported sequence (8 samples) find no period (the
-  // oracle rejects them too)
-  std::vector<int32_t> run_trace, run_start, run_seg, run_len;
-  for (size_t i = 0; i < sfx_trace.size(); ++i) {
-    const int32_t Nt = host_len ? host_len[sfx_trace[i]] : N;
-    if (Nt - sfx_start[i] >= (1 << GPOEO_MIN_LOG2N)) {
-      run_trace.push_back(sfx_trace[i]);
-      run_start.push_back(sfx_start[i]);
-      run_seg.push_back((int32_t)i);
-      run_len.push_back(Nt - sfx_start[i]);
-    }
-  }
-  const int64_t nrun = (int64_t)run_seg.size();
-  std::vector<int32_t> hn;
-  for (int64_t c0 = 0; c0 < nrun; c0 += batch) {
-    const int32_t n = (int32_t)(nrun - c0 < batch ? nrun - c0 : batch);
-    hn.resize(n);
-    int32_t Smax = 0;
-    for (int32_t r = 0; r < n; ++r) {
-      hn[r] = run_len[c0 + r];
-      if (hn[r] > Smax) Smax = hn[r];
-    }
-    const int32_t S = (Smax + 3) & ~3;
-    const gpoeo_params q = suffix_params(p, S);
-    if (q.min_period > q.max_period) continue;  // every row too short for L_min: no period (as the oracle)
-    CK(cudaMemcpyAsync(gtrace, run_trace.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(gstart, run_start.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(grown, hn.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(gseg, run_seg.data() + c0, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
-    CK(launch_gather_suffix_ragged(y, N, gtrace, gstart, grown, n, S, gsig, s));
-    Plan pr = make_plan(&q, n);
-    pr.row_n = grown;
-    pr.max_local = (int64_t)q.max_period - q.min_period + 1;  // rows clip L_max to N_j/2: bound
-    const Layout Lr = layout(pr);
-    if (Lr.total > R.total - R.gws) return GPOEO_ERR_WORKSPACE;  // not expected: R.gws bounds it
-    if (band_smem_bytes(pr, false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
+  // lines 2-13: the suffix plan, on the device
+  CK(launch_rolling_plan(batch, N, dev_len, whole, rpd, (int32_t)R.max_sub, dplan, gstart, glen, s));
+  // line 11: Alg. 1 on every suffix, as a one-channel sequence of its own length
+  gpoeo_params q;
+  Plan pr = suffix_plan(p, batch, &q);
+  const int32_t S = q.n_samples;
+  const Layout Lr = layout(pr);
+  for (int64_t j = 0; j < R.max_sub; ++j) {
+    const int32_t* lj = glen + j * batch;
+    CK(launch_gather_suffix_ragged(y, N, nullptr, gstart + j * batch, lj, (int32_t)batch, S, gsig, s));
+    pr.row_n = lj;
     rc = run_detect(gsig, pr, Lr, b + R.gws, gres, gdet, s);
     if (rc != GPOEO_OK) return rc;
-    CK(launch_scatter_suffix(gres, gdet, n, gseg, dsegs, s));
-    // the host vectors are rewritten by the next chunk: pageable H2D copies are staged before
-    // cudaMemcpyAsync returns
+    CK(launch_scatter_suffix(gres, gdet, (int32_t)batch, nullptr, (int32_t)R.max_sub, (int32_t)j, dsegs, s));
   }
   // lines 14-21
-  RollParamsDev rpd{rp->c_measure, rp->step, rp->c_eval, rp->diff_threshold};
-  CK(launch_rolling_final(batch, N, host_len ? dev_len : nullptr, p->sample_interval, rpd, whole, dplan, dsegs,
-                          results, s));
-  CK(cudaStreamSynchronize(s));
+  CK(launch_rolling_final(batch, N, dev_len, p->sample_interval, rpd, whole, dplan, dsegs, results, s));
   return GPOEO_OK;
 }
 
@@ -699,7 +639,8 @@ int gpoeo_detect_rolling(const float* traces, int64_t batch, const gpoeo_params*
   if ((batch > 0 && !aligned16(traces)) || !aligned16(workspace)) return GPOEO_ERR_MISALIGNED;
   if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
   if (batch == 0) return GPOEO_OK;
-  return rolling_core(traces, batch, p, rp, nullptr, nullptr, nullptr, results, static_cast<char*>(workspace), R,
+  if (band_smem_bytes(suffix_plan(p, batch, nullptr), false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
+  return rolling_core(traces, batch, p, rp, nullptr, nullptr, results, static_cast<char*>(workspace), R,
                       static_cast<cudaStream_t>(stream));
 }
 
@@ -747,6 +688,7 @@ int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_param
   if (check_device() != GPOEO_OK) return GPOEO_ERR_CUDA;
   if (batch == 0) return GPOEO_OK;
   if (band_smem_bytes(main_plan(p, batch, true), false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
+  if (band_smem_bytes(suffix_plan(p, batch, nullptr), false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   char* b = static_cast<char*>(workspace);
   int32_t* dlen = reinterpret_cast<int32_t*>(b + M.len);
@@ -772,10 +714,12 @@ int gpoeo_measure_adaptive(const float* traces, int64_t batch, const gpoeo_param
     for (int32_t i = 0; i < na; ++i) alen[i] = n[act[i]];
     CK(cudaMemcpyAsync(dlen, alen.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(didx, act.data(), sizeof(int32_t) * na, cudaMemcpyHostToDevice, s));
-    int rc = rolling_core(traces, na, p, rp, alen.data(), dlen, didx, dres, b, M.R, s);
+    int rc = rolling_core(traces, na, p, rp, dlen, didx, dres, b, M.R, s);
     if (rc != GPOEO_OK) return rc;
     hr.resize(na);
-    CK(cudaMemcpy(hr.data(), dres, sizeof(gpoeo_rolling_result) * na, cudaMemcpyDeviceToHost));
+    // the one host read of the round: every session's SmpDur_next decides the next round
+    CK(cudaMemcpyAsync(hr.data(), dres, sizeof(gpoeo_rolling_result) * na, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     std::vector<int32_t> next;
     for (int32_t i = 0; i < na; ++i) {
       const int32_t t = act[i];

@@ -189,7 +189,10 @@ struct RollParamsDev {
 cudaError_t launch_gather_suffix_ragged(const float* y, int32_t N, const int32_t* trace, const int32_t* start,
                                         const int32_t* len, int32_t n, int64_t stride, float* dst, cudaStream_t s);
 cudaError_t launch_scatter_suffix(const gpoeo_result* res, const gpoeo_detail* det, int32_t n, const int32_t* seg,
-                                  RollSeg* out, cudaStream_t s);
+                                  int32_t seg_stride, int32_t seg_off, RollSeg* out, cudaStream_t s);
+cudaError_t launch_rolling_plan(int64_t batch, int32_t N, const int32_t* row_n, const gpoeo_result* whole,
+                                RollParamsDev rp, int32_t max_sub, RollTrace* plan, int32_t* start, int32_t* len,
+                                cudaStream_t s);
 cudaError_t launch_rolling_final(int64_t batch, int32_t N, const int32_t* row_n, double Ts, RollParamsDev rp,
                                  const gpoeo_result* whole, const RollTrace* plan, const RollSeg* segs,
                                  gpoeo_rolling_result* out, cudaStream_t s);
