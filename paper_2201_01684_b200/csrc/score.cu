@@ -492,11 +492,18 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 // label changed" is exact. The final W_i / W_{i+1} pass walks the slots in one order for
 // both windows (Z28). Decisions equal the per-sample evaluation except at sub-rounding
 // margins (Z27). Cost per pass: O(K + straddled samples) instead of O(L).
+// VS (the mid launch): the sort stores the values themselves in slot order, so the bucket
+// sums and the straddling members read shared memory (no gathers), a straddling bucket is
+// evaluated 32 slots per warp step (no flattened member list), labels are kept per slot, and
+// the final pass gives a member of a mixed bucket the per-sample rule's label of its value.
 #ifndef GPOEO_BUCKETS
 #define GPOEO_BUCKETS 32
 #endif
 #ifndef GPOEO_BUCKET_MINB
 #define GPOEO_BUCKET_MINB 14  // resident one-warp CTAs per SM the register budget targets (xl launch)
+#endif
+#ifndef GPOEO_MID_VS
+#define GPOEO_MID_VS 1  // mid launch: window values in shared memory (else 16-bit positions + gathers)
 #endif
 #ifndef GPOEO_BUCKET_MINB_MID
 #define GPOEO_BUCKET_MINB_MID 20  // the same for the mid launch (L <= kBucketSplitL, smaller regions)
@@ -518,15 +525,17 @@ __host__ __device__ constexpr size_t bucket_labcnt_bytes(int Lcap) {
   return (((size_t)Lcap + 15) & ~(size_t)15) > (size_t)kBuckets * 32 * 2 ? (((size_t)Lcap + 15) & ~(size_t)15)
                                                                           : (size_t)kBuckets * 32 * 2;
 }
-__host__ __device__ constexpr size_t bucket_region_bytes(int Lcap) {
-  return (((size_t)Lcap * 2 + 15) & ~(size_t)15) + bucket_labcnt_bytes(Lcap) + (size_t)kBuckets * 8 * 2 +
+// VS (values in shared memory): the slot array holds the values (4 B) instead of positions
+__host__ __device__ constexpr size_t bucket_region_bytes(int Lcap, bool VS = false) {
+  return (((size_t)Lcap * (VS ? 4 : 2) + 15) & ~(size_t)15) + bucket_labcnt_bytes(Lcap) + (size_t)kBuckets * 8 * 2 +
          (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 4 + kBuckets +
          (size_t)kBuckets * 4 + 64;
 }
 
 struct BucketView {
   uint16_t* pos;   // [Lcap] sorted slot -> sample index in the window
-  uint8_t* lab;    // [Lcap] current label of each sample (by position in the window)
+  float* val;      // [Lcap] VS: sorted slot -> sample value (aliases pos)
+  uint8_t* lab;    // [Lcap] current label of each sample (by position in the window; VS: by slot)
   double* s1;      // [K]   sum (y - c_b)
   double* s2;      // [K]   sum (y - c_b)^2
   float* bmin;     // [K]
@@ -538,11 +547,12 @@ struct BucketView {
   uint8_t* blab;   // [K]   bucket state: l < G every member has label l; 0xFF mixed (lab[]); 0xFE unset
   uint32_t* seen;  // [K]   labels seen among a straddling bucket's members this pass (bit mask)
 
-  __device__ static BucketView carve(uint8_t* base, int Lcap) {
+  __device__ static BucketView carve(uint8_t* base, int Lcap, bool VS = false) {
     BucketView v;
     uint8_t* p = base;
     v.pos = reinterpret_cast<uint16_t*>(p);
-    p += ((size_t)Lcap * 2 + 15) & ~(size_t)15;
+    v.val = reinterpret_cast<float*>(p);
+    p += ((size_t)Lcap * (VS ? 4 : 2) + 15) & ~(size_t)15;
     v.lab = p;
     v.lcnt = reinterpret_cast<uint16_t*>(p);
     p += bucket_labcnt_bytes(Lcap);
@@ -599,7 +609,7 @@ __device__ __forceinline__ void score_crossings(double muj, double cj, double hj
 
 // have_range: range = [min, max] of W_i, already seen by the previous pair's final pass; on
 // return range = [min, max] of W_{i+1} (this pair's final pass reads it), for the next pair.
-template <int G>
+template <int G, bool VS>
 __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int lane, BucketView bv, int maxit,
                                   long long& passes_out, bool have_range, float2& range) {
   constexpr int NV = 3 * G + 1;
@@ -703,10 +713,12 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   }
 #pragma unroll 4
   for (int s = lane; s < L; s += 32) {
-    const int b = bucket_of(s);
+    const float v = __ldg(A + s);
+    const int b = bucket_of_v(v);
     const int slot = bv.lcnt[b * 32 + lane];
     bv.lcnt[b * 32 + lane] = (uint16_t)(slot + 1);
-    bv.pos[slot] = (uint16_t)s;
+    if (VS) bv.val[slot] = v;
+    else bv.pos[slot] = (uint16_t)s;
   }
   __syncwarp();
   GPOEO_TICK(8, tk);
@@ -719,10 +731,10 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     float lo = INFINITY, hi = -INFINITY, c = 0.f;
     double a1 = 0.0, a2 = 0.0;
     if (i1 > i0) {
-      c = __ldg(A + bv.pos[i0]);
+      c = VS ? bv.val[i0] : __ldg(A + bv.pos[i0]);
 #pragma unroll 4
       for (int i = i0; i < i1; ++i) {
-        const float v = __ldg(A + bv.pos[i]);
+        const float v = VS ? bv.val[i] : __ldg(A + bv.pos[i]);
         lo = fminf(lo, v);
         hi = fmaxf(hi, v);
         const double d = (double)v - (double)c;
@@ -859,6 +871,40 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       changed |= (int)(bv.blab[b] != lbl);  // 0xFF (mixed) -> l changes some member
       bv.blab[b] = (uint8_t)lbl;
     }
+    if constexpr (VS) {
+      // straddling buckets one at a time, 32 slots per warp step, values from shared memory
+      // (no gathers, no member list); labels kept per slot
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) {
+#pragma unroll 1
+        for (unsigned sb = __ballot_sync(FULL, need[q] != 0); sb; sb &= sb - 1u) {
+          const int b = (__ffs(sb) - 1) + 32 * q;
+          const int o0 = bv.off[b], o1 = bv.off[b + 1];
+          const int st = bv.blab[b];  // previous state: uniform label, or mixed (per slot)
+          int first = -1;
+          bool uni = true;
+#pragma unroll 1
+          for (int c = o0; c < o1; c += 32) {
+            const int slot = c + lane;
+            const bool ok = slot < o1;
+            const double y = ok ? (double)bv.val[slot] : 0.0;
+            double e[G];
+            const int lbl = cem.assign(y, it, e);
+            if (ok) {
+#pragma unroll
+              for (int j = 0; j < G; ++j)
+                if (lbl == j) { nc[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
+              const int old = st < G ? st : (int)bv.lab[slot];
+              changed |= (int)(old != lbl);
+              bv.lab[slot] = (uint8_t)lbl;
+            }
+            if (first < 0) first = __shfl_sync(FULL, lbl, 0);  // slot o0 (< o1) is lane 0's
+            uni &= __all_sync(FULL, !ok || lbl == first);
+          }
+          if (lane == 0) bv.blab[b] = (uint8_t)(uni ? first : 0xFF);
+        }
+      }
+    } else {
     // flattened member list of the straddling buckets: (exclusive member offset << 8) | bucket
     int mine = 0;
 #pragma unroll
@@ -936,6 +982,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
           bv.blab[b] = (uint8_t)((sm & (sm - 1)) ? 0xFF : (__ffs(sm) - 1));
         }
     }
+    }  // VS
     __syncwarp();
     passes = it;
 #if GPOEO_BUCKET_RS
@@ -985,7 +1032,14 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     TA += ya;
     w[3 * G] += yb;
     int l = bv.blab[bucket_of_v(fa)];
-    if (l >= G) l = bv.lab[p];
+    if (l >= G) {
+      if (VS) {  // mixed bucket: the per-sample rule of the last pass gave this value's slot its label
+        double e[G];
+        l = cem.assign(ya, passes, e);
+      } else {
+        l = bv.lab[p];
+      }
+    }
 #pragma unroll
     for (int j = 0; j < G; ++j)
       if (l == j) { w[j] += 1.0; w[G + j] += ya; w[2 * G + j] += yb; }
@@ -1167,7 +1221,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
 
 // Bucket path (L >= kBucketMinL): kBucketWarps warps per CTA, one query per CTA at a
 // time, one pair per warp at a time (streaming path beyond bucket_lcap).
-template <int G, int MINB>
+template <int G, int MINB, bool VS>  // VS: bucketed with the values in shared memory (mid launch)
 __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(ScoreArgs a) {
   __shared__ int64_t s_item;
   __shared__ double s_team[kBucketWarps];
@@ -1188,11 +1242,12 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
     const float* yt = a.y + t * a.ystride;
     double acc = 0.0;
     if (L <= a.bucket_lcap) {
-      BucketView bv = BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap), a.bucket_lcap);
+      BucketView bv =
+          BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap, VS), a.bucket_lcap, VS);
       float2 range = make_float2(0.f, 0.f);
       for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
         // kBucketWarps == 1: pairs in order, so the previous final pass saw this W_i
-        acc += pair_err_bucket<G>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes, pidx != warp, range);
+        acc += pair_err_bucket<G, VS>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes, pidx != warp, range);
         __syncwarp();
       }
     } else {
@@ -1231,11 +1286,11 @@ static int grid_of(K kern, int threads, size_t smem, int cap) {
   return g < cap ? g : cap;
 }
 
-template <int G, int MINB>
+template <int G, int MINB, bool VS>
 static cudaError_t launch_bucket(ScoreArgs a, int lcap, cudaStream_t s) {
   a.bucket_lcap = lcap;
-  const size_t smem = (size_t)kBucketWarps * bucket_region_bytes(lcap);
-  auto kern = score_bucket_kernel<G, MINB>;
+  const size_t smem = (size_t)kBucketWarps * bucket_region_bytes(lcap, VS);
+  auto kern = score_bucket_kernel<G, MINB, VS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // label-scratch slots exist for kMaxScoreCtas * kWarps warps (gpoeo_api.cu layout)
@@ -1252,7 +1307,7 @@ static cudaError_t launch_xl(const ScoreArgs& base, const ItemList& list, int32_
   a.count = list.n_xl;
   a.cursor = list.cur_xl;
   a.reverse = 0;
-  return launch_bucket<G, GPOEO_BUCKET_MINB>(a, ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15, s);
+  return launch_bucket<G, GPOEO_BUCKET_MINB, false>(a, ((max_L < kBucketMaxL ? max_L : kBucketMaxL) + 15) & ~15, s);
 }
 
 template <int G>
@@ -1264,7 +1319,9 @@ static cudaError_t launch_mid(const ScoreArgs& base, const ItemList& list, int32
   a.cursor = list.cur_big;
   a.reverse = 1;
   const int top = max_L < kBucketSplitL ? max_L : kBucketSplitL;
-  return launch_bucket<G, GPOEO_BUCKET_MINB_MID>(a, (top + 15) & ~15, s);
+  // values in shared memory for the mid launch (8 KB of values at L = 2048 still leave 18
+  // warps per SM); the xl launch keeps 16-bit positions (its windows would need 32 KB)
+  return launch_bucket<G, GPOEO_BUCKET_MINB_MID, GPOEO_MID_VS != 0>(a, (top + 15) & ~15, s);
 }
 
 template <int G>
