@@ -901,6 +901,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
             if (first < 0) first = __shfl_sync(FULL, lbl, 0);  // slot o0 (< o1) is lane 0's
             uni &= __all_sync(FULL, !ok || lbl == first);
           }
+          __syncwarp();  // every lane has read the old state
           if (lane == 0) bv.blab[b] = (uint8_t)(uni ? first : 0xFF);
         }
       }

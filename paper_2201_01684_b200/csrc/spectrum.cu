@@ -677,8 +677,8 @@ struct FusedShared {
   // cluster hand-offs without cluster barriers (one phase per trace each):
   uint64_t mb_stat;  // the partner's stats landed here (st.async, complete_tx)
   uint64_t mb_dif;   // the partner's DIF half landed in my buffer (st.async, complete_tx)
-  uint64_t mb_p;     // the partner's P is complete (remote arrive)
-  uint64_t mb_free;  // the partner finished reading my buffer (remote arrive; phase 0 at start)
+  uint64_t mb_p;     // the partner's P landed in my Prx (st.async, complete_tx)
+  uint64_t mb_free;  // the partner finished reading its buffers: I may push into them (relaxed remote arrive)
 };
 
 // mbarrier / DSMEM helpers (PTX): the partner CTA's data arrives by st.async with
@@ -701,11 +701,29 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_remote_arrive(uint32_t remote_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
 }
+// "my reads of the buffers are done" (a write-after-read hand-off: the reads have returned
+// their values before the CTA barrier that precedes this, so no release fence is needed)
+__device__ __forceinline__ void mbar_remote_arrive_relaxed(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
+__device__ __forceinline__ void st_async_f4(uint32_t remote_addr, float4 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   remote_addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_f1(uint32_t remote_addr, float v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(remote_addr), "f"(v),
+               "r"(remote_bar)
+               : "memory");
+}
+// data hand-offs arrive by st.async (async proxy, complete_tx on my own barrier): a CTA-scope
+// wait sees them (no cluster-scope acquire, whose L1 invalidation costs every wait)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok = 0;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
@@ -722,7 +740,14 @@ __device__ __forceinline__ void st_async_b64(uint32_t remote_addr, double v, uin
                "l"(__double_as_longlong(v)), "r"(remote_bar)
                : "memory");
 }
-constexpr size_t kDynSmem = (size_t)kBuf * sizeof(float2) + (size_t)kTw * sizeof(float2);
+// [buf: kBuf float2 (Z, then my P in place)] [tw] [Prx: the partner's bins that my in-band
+// bins neighbour: partner-local indices [prx_lo, prx_hi], prx_lo a multiple of 4]
+__host__ __device__ __forceinline__ int prx_lo(int k_lo) { return (k_lo - 2 > 0 ? (k_lo - 2) >> 1 : 0) & ~3; }
+__host__ __device__ __forceinline__ int prx_hi(int k_hi) { return ((k_hi + 2) >> 1) < kn2 ? ((k_hi + 2) >> 1) : kn2; }
+__host__ __device__ __forceinline__ size_t dyn_smem(int k_lo, int k_hi) {
+  const int n = prx_hi(k_hi) - prx_lo(k_lo) + 1;
+  return (size_t)kBuf * sizeof(float2) + (size_t)kTw * sizeof(float2) + (size_t)((n > 0 ? n : 0) + 8) * sizeof(float);
+}
 
 // P[k] of the full spectrum held contiguously in shared memory, mirrored edges (Z5)
 __device__ __forceinline__ float pget(const float* P, int k) {
@@ -794,7 +819,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
   cg::cluster_group cluster = cg::this_cluster();
   const int q = (int)cluster.block_rank();
   const int cid = blockIdx.x / 2;
-  float2* pbuf = cluster.map_shared_rank(buf, q ^ 1);
+  float* Prx = reinterpret_cast<float*>(buf + kBuf + kTw);  // the partner's bins [mlo, recv_hi] (pushed to me)
+  const int mlo = prx_lo(p.k_lo);
+  const int push_hi = prx_hi(p.k_hi) < (q == 0 ? kn2 : kn2 - 1) ? prx_hi(p.k_hi) : (q == 0 ? kn2 : kn2 - 1);
+  const int recv_hi = prx_hi(p.k_hi) < (q == 1 ? kn2 : kn2 - 1) ? prx_hi(p.k_hi) : (q == 1 ? kn2 : kn2 - 1);
   FusedShared* pfs = cluster.map_shared_rank(&fs, q ^ 1);
   FusedShared* fs0 = cluster.map_shared_rank(&fs, 0);
   for (int m = threadIdx.x; m < kTw; m += kT) {
@@ -823,13 +851,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
   // memory is written: one cluster barrier per launch (racecheck: "block that might not have
   // entered yet")
   cluster.sync();
-  if (threadIdx.x == 0) mbar_remote_arrive(mapa_u32(mb_free, partner));  // my buffer is free (phase 0)
+  if (threadIdx.x == 0) mbar_remote_arrive_relaxed(mapa_u32(mb_free, partner));  // my buffers are free (phase 0)
   const uint32_t rbuf = mapa_u32(smem_u32(buf), partner);  // the partner's buffer in the cluster window
   const bool exact_y = y_out != nullptr || mode != kPeaksMajor;
   uint32_t par = 0;  // phase parity of the per-trace barriers
   for (int64_t t = cid; t < p.batch; t += nclusters, par ^= 1u) {
     const float* xt = x + t * p.stride;
-    if (threadIdx.x == 0) mbar_arrive_expect_tx(mb_stat, 16u * F);  // the partner's 2F doubles
+    if (threadIdx.x == 0) {
+      mbar_arrive_expect_tx(mb_stat, 16u * F);  // the partner's 2F doubles
+      mbar_arrive_expect_tx(mb_p, 4u * (uint32_t)(recv_hi >= mlo ? recv_hi - mlo + 1 : 0));  // its bins
+    }
 #ifdef GPOEO_FZ_TIMING
     long long fz_t0 = clock64();
 #endif
@@ -959,7 +990,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
 #if GPOEO_FZ_PREFETCH == 2
     if (t + nclusters < p.batch) prefetch_half<F>(x + (t + nclusters) * p.stride, q);
 #endif
-    mbar_wait(mb_free, par);  // the partner finished reading my buffer (previous trace's phase E)
+    mbar_wait(mb_free, par);  // the partner finished reading its buffers (previous trace's phase E)
     FZ_T(2);
     if (threadIdx.x == 0) mbar_arrive_expect_tx(mb_dif, (uint32_t)(kn2 / 2) * 8u);  // the partner's half
     const uint32_t rbar_dif = mapa_u32(mb_dif, partner);
@@ -1022,7 +1053,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     FZ_T(5);
     // ---- D: R2C post: P[2 k2 + q] (C = 2: partner bins sit in the same CTA) ------------
     float* P = reinterpret_cast<float*>(buf);
-    const float* Pp = reinterpret_cast<const float*>(pbuf);
+    const float* Pp = Prx - mlo;  // the partner's bins by partner-local index (valid in [mlo, recv_hi])
 #if GPOEO_R2C_PAIR
     // bins k and k' = n - k (same parity, so the same CTA) share Z_k, Z_{n-k}: E' = conj(E),
     // O' = conj(O), W' = -conj(W), hence X' = conj(E - W O): one pair of loads, one twiddle
@@ -1112,7 +1143,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
 #endif
     if (mode == kPeaksCandidates && q == 0 && threadIdx.x == 0) fs.ps.count = 0;
     __syncthreads();  // my P is complete: announce it to the partner (its phase E reads my bins)
-    if (threadIdx.x == 0) mbar_remote_arrive(mapa_u32(mb_p, partner));
+    // push the bins the partner's in-band bins neighbour into its Prx: 16-B st.async with
+    // complete_tx on its barrier -- no fence, and no remote read in phase E
+    {
+      const uint32_t rprx = mapa_u32(smem_u32(Prx), partner), rbar_p = mapa_u32(mb_p, partner);
+      const int n = push_hi - mlo + 1;  // my bins [mlo, push_hi]
+      for (int e = 4 * threadIdx.x; e + 4 <= n; e += 4 * kT)
+        st_async_f4(rprx + (uint32_t)e * 4u, *reinterpret_cast<const float4*>(P + mlo + e), rbar_p);
+      if ((int)threadIdx.x < (n & 3)) {
+        const int e = (n & ~3) + (int)threadIdx.x;
+        st_async_f1(rprx + (uint32_t)e * 4u, P[mlo + e], rbar_p);
+      }
+    }
     FZ_T(6);
     mbar_wait(mb_p, par);  // the partner's P is complete
     FZ_T(7);
@@ -1163,8 +1205,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       }
 #if GPOEO_MAJOR_SPLIT
       if (mode == kPeaksMajor) {
-        __syncthreads();  // every read of both buffers for this trace is done
-        if (threadIdx.x == 0) mbar_remote_arrive(mapa_u32(mb_free, partner));
+        __syncthreads();  // every read of my buffers for this trace is done
+        if (threadIdx.x == 0) mbar_remote_arrive_relaxed(mapa_u32(mb_free, partner));
         continue;
       }
 #endif
@@ -1212,7 +1254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     // every read of both buffers for this trace is done: the partner may overwrite my buffer
     // (its next phase B waits for this)
     __syncthreads();
-    if (threadIdx.x == 0) mbar_remote_arrive(mapa_u32(mb_free, partner));
+    if (threadIdx.x == 0) mbar_remote_arrive_relaxed(mapa_u32(mb_free, partner));
   }
   cluster.sync();  // the partner may still read my shared memory: do not exit before it is done
 }
@@ -1221,11 +1263,12 @@ template <int F>
 static cudaError_t launch_fused_65536(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
                                       int mode, cudaStream_t s) {
   auto kern = fused_spectrum_65536<F>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fz::kDynSmem);
+  const size_t smem = fz::dyn_smem(p.k_lo, p.k_hi);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(fz::kT);
-  cfg.dynamicSmemBytes = fz::kDynSmem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.gridDim = dim3(2);
   int nclust = 0;
