@@ -247,7 +247,7 @@ __host__ __device__ constexpr int team_rs_min() {
 template <int G>
 __device__ __forceinline__ void team_reduce_mstep(Cem<G>& cem, const double* v, const int32_t* n, int changed,
                                                   bool& active, int& passes, int it, int maxit, int L, int tau,
-                                                  int lane) {
+                                                  int lane, double* prm = nullptr) {
   constexpr int H = team_rs_h<G>();
   constexpr int NVR = 1 << H;
   constexpr int NPK = (G + 1) / 2;
@@ -306,6 +306,11 @@ __device__ __forceinline__ void team_reduce_mstep(Cem<G>& cem, const double* v, 
       c = 0.5 * log(2.0 * pp * pp * h);  // ln pi - 1/2 ln var
     }
   }
+  if (prm && j < G && lt == (j << sh)) {  // the bucketed warp's table: (mu, c, h) of component j
+    prm[j] = mu;
+    prm[8 + j] = c;
+    prm[16 + j] = h;
+  }
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     const int src = base + (k << sh);
@@ -313,6 +318,7 @@ __device__ __forceinline__ void team_reduce_mstep(Cem<G>& cem, const double* v, 
     cem.c[k] = __shfl_sync(FULL, c, src);
     cem.h[k] = __shfl_sync(FULL, h, src);
   }
+  if (prm) __syncwarp();  // the table is visible to the next pass's root lanes
 }
 
 // ---------------------------------------------------------------------------------
@@ -529,7 +535,7 @@ __host__ __device__ constexpr size_t bucket_labcnt_bytes(int Lcap) {
 __host__ __device__ constexpr size_t bucket_region_bytes(int Lcap, bool VS = false) {
   return (((size_t)Lcap * (VS ? 4 : 2) + 15) & ~(size_t)15) + bucket_labcnt_bytes(Lcap) + (size_t)kBuckets * 8 * 2 +
          (size_t)kBuckets * 4 * 3 + (size_t)(kBuckets + 8) * 2 + (size_t)kBuckets * 4 + kBuckets +
-         (size_t)kBuckets * 4 + 64;
+         (size_t)kBuckets * 4 + 64 + 3 * 8 * 8;
 }
 
 struct BucketView {
@@ -546,6 +552,7 @@ struct BucketView {
   uint16_t* lcnt;  // [K][32] per-lane bucket counts / scatter cursors of the counting sort (aliases lab)
   uint8_t* blab;   // [K]   bucket state: l < G every member has label l; 0xFF mixed (lab[]); 0xFE unset
   uint32_t* seen;  // [K]   labels seen among a straddling bucket's members this pass (bit mask)
+  double* prm;     // [3][8] this pass's (mu, c, h) by component: the root lanes read their pair's
 
   __device__ static BucketView carve(uint8_t* base, int Lcap, bool VS = false) {
     BucketView v;
@@ -573,6 +580,9 @@ struct BucketView {
     v.blab = p;
     p += ((size_t)kBuckets + 3) & ~(size_t)3;
     v.seen = reinterpret_cast<uint32_t*>(p);
+    p += (size_t)kBuckets * 4;
+    p = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 7) & ~(uintptr_t)7);
+    v.prm = reinterpret_cast<double*>(p);
     return v;
   }
 };
@@ -754,6 +764,8 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // ---- CEM passes --------------------------------------------------------------------
   Cem<G> cem;
   cem.init(mn, R);
+  if (lane < G) bv.prm[lane] = __dadd_rn(mn, __dmul_rn((double)lane + 0.5, R / (double)G));  // = cem.mu[lane]
+  __syncwarp();
   const double delta = 1e-6 * R;
   // root slot x = lane + 32 t (t < RPL) is root (x & 1) of component pair x >> 1
   constexpr int RPL = (2 * P + 31) / 32 > 0 ? (2 * P + 31) / 32 : 1;
@@ -784,12 +796,9 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     for (int t = 0; t < RPL; ++t) {
       const int x = lane + 32 * t;
       double r0 = NAN, r1 = NAN;
-      double muj = 0, cj = 0, hj = 0, muk = 0, ck = 0, hk = 0;
-#pragma unroll
-      for (int j = 0; j < G; ++j) {
-        if (j == pj[t]) { muj = cem.mu[j]; cj = cem.c[j]; hj = cem.h[j]; }
-        if (j == pk[t]) { muk = cem.mu[j]; ck = cem.c[j]; hk = cem.h[j]; }
-      }
+      // the pair's parameters from the warp's table (one load each, no select chains)
+      double muj = bv.prm[pj[t]], cj = bv.prm[8 + pj[t]], hj = bv.prm[16 + pj[t]];
+      double muk = bv.prm[pk[t]], ck = bv.prm[8 + pk[t]], hk = bv.prm[16 + pk[t]];
       if (it == 1) { cj = ck = 0.0; hj = hk = 1.0; }  // first pass: argmin (y - mu)^2
       if (x < 2 * P && (x & 1) == 0) score_crossings(muj, cj, hj, muk, ck, hk, mn, r0, r1);
       const double r1_left = __shfl_up_sync(FULL, r1, 1);
@@ -989,7 +998,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
 #if GPOEO_BUCKET_RS
     // the last pass needs no sums (the final pass below recomputes the groups' statistics)
     bool act = true;
-    team_reduce_mstep<G>(cem, v, nc, changed, act, passes, it, maxit, L, 32, lane);
+    team_reduce_mstep<G>(cem, v, nc, changed, act, passes, it, maxit, L, 32, lane, bv.prm);
     if (!act) break;  // labels final
 #else
     const bool any_changed = __any_sync(FULL, changed);
