@@ -566,6 +566,10 @@ static cudaError_t launch_spec_t(const Plan& p, const float* y, const int32_t* s
 #ifndef GPOEO_FZ_PREFETCH
 #define GPOEO_FZ_PREFETCH 1  // L2 prefetch of the next trace: 0 none, 1 after phase B, 2 after phase A
 #endif
+#ifndef GPOEO_FZ_BUNROLL
+#define GPOEO_FZ_BUNROLL 8  // spectral-only phase B: j-values per thread whose loads are in flight together
+#endif
+constexpr int kBUnroll = GPOEO_FZ_BUNROLL;
 #ifndef GPOEO_FZ_A_ALLLOADS
 #define GPOEO_FZ_A_ALLLOADS 0
 #endif
@@ -675,6 +679,8 @@ __device__ __forceinline__ void pass(float2* buf, const float2* tw, int Ns) {
 
 struct FusedShared {
   PeakShared ps;
+  double cm[GPOEO_MAX_FEATURES], ca[GPOEO_MAX_FEATURES];  // this trace's channel means and weights
+  int32_t cs[GPOEO_MAX_FEATURES];                          // sigma_c > 0
   double red[kT / 32 * 2 * GPOEO_MAX_FEATURES];
   double stat[2][2][GPOEO_MAX_FEATURES][2];  // [trace parity][rank][channel][sum, shifted sum of squares]
   float pm[2];                               // per-rank in-band peak maximum
@@ -964,10 +970,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     __syncthreads();
     mbar_wait(mb_stat, par);
     FZ_T(1);
-    bool all_const = true;
-    double m[F], a[F];
-#pragma unroll
-    for (int c = 0; c < F; ++c) {
+    // channel c's mean and weight on thread c (one sqrt and one division per channel, not per
+    // thread), shared through shared memory
+    if (threadIdx.x < F) {
+      const int c = threadIdx.x;
       const double x0 = (double)__ldg(xt + (int64_t)c * kN);
       const double s = fs.stat[par][0][c][0] + fs.stat[par][1][c][0];
       const double qq = fs.stat[par][0][c][1] + fs.stat[par][1][c][1];
@@ -976,9 +982,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
       double var = qq / (double)kN - dm * dm;
       if (!(var > 0.0)) var = 0.0;
       const double sigma = sqrt(var);
-      m[c] = mu;
-      a[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
-      if (sigma > 0.0) all_const = false;
+      fs.cm[c] = mu;
+      fs.ca[c] = sigma > 0.0 ? (double)p.w[c] / sigma : 0.0;
+      fs.cs[c] = sigma > 0.0 ? 1 : 0;
+    }
+    __syncthreads();
+    bool all_const = true;
+    double m[F], a[F];
+#pragma unroll
+    for (int c = 0; c < F; ++c) {
+      m[c] = fs.cm[c];
+      a[c] = fs.ca[c];
+      if (fs.cs[c]) all_const = false;
     }
     // ---- B: signal + DIF split into the two CTAs' buffers ------------------------------
     // exact_y (the scorer or the debug surface reads y): y = fp32(fp64 channel-order sum of
@@ -1002,11 +1017,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     FZ_T(2);
     if (threadIdx.x == 0) mbar_arrive_expect_tx(mb_dif, (uint32_t)(kn2 / 2) * 8u);  // the partner's half
     const uint32_t rbar_dif = mapa_u32(mb_dif, partner);
+    // the DIF butterfly of one j: a_0 = z[j] + z[j + n2] here, a_1 = (z[j] - z[j + n2]) W^j to
+    // the partner (or the other way round on rank 1)
+    // W_32768^j along a thread's j = j0 + 512 u: one product by W_64 per step from the table
+    // value at j0 (16 steps: error ~1e-6, inside the 1e-4 spectrum bar, Z29)
+    const int j0 = q * (kn2 / 2) + (int)threadIdx.x;
+    float2 wj = twiddle(tw, j0 >> 1);  // W_32768^j = W_16384^(j/2) (x W_32768 if j odd)
+    if (j0 & 1) wj = cmul(wj, w32768);
+    const float2 w64 = make_float2(9.951847266722e-01f, -9.801714032956e-02f);  // W_32768^512
+    auto dif_store = [&](int j, float2 za, float2 zb) {
+      const float2 a0 = cadd(za, zb);
+      const float2 a1 = cmul(csub(za, zb), wj);
+      wj = cmul(wj, w64);
+      buf[pad(j)] = q == 0 ? a0 : a1;
+      st_async_f2(rbuf + (uint32_t)pad(j) * 8u, q == 0 ? a1 : a0, rbar_dif);
+    };
+    if (exact_y) {
 #pragma unroll 4
-    for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
-      const int j = q * (kn2 / 2) + jj;
-      float2 za, zb;
-      if (exact_y) {
+      for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
+        const int j = q * (kn2 / 2) + jj;
         double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
 #pragma unroll
         for (int c = 0; c < F; ++c) {
@@ -1019,15 +1048,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
           yb0 = __dadd_rn(yb0, __dmul_rn(a[c], __dsub_rn((double)xb.x, m[c])));
           yb1 = __dadd_rn(yb1, __dmul_rn(a[c], __dsub_rn((double)xb.y, m[c])));
         }
-        za = make_float2(__double2float_rn(ya0), __double2float_rn(ya1));
-        zb = make_float2(__double2float_rn(yb0), __double2float_rn(yb1));
+        const float2 za = make_float2(__double2float_rn(ya0), __double2float_rn(ya1));
+        const float2 zb = make_float2(__double2float_rn(yb0), __double2float_rn(yb1));
         if (yt) {
           reinterpret_cast<float2*>(yt)[j] = za;
           reinterpret_cast<float2*>(yt + kn)[j] = zb;
         }
-      } else {
-        za = make_float2(-b32, -b32);
-        zb = za;
+        dif_store(j, za, zb);
+      }
+    } else {
+      // straight-line body: GPOEO_FZ_BUNROLL j-values' loads in flight per thread
+#pragma unroll kBUnroll
+      for (int jj = threadIdx.x; jj < kn2 / 2; jj += kT) {
+        const int j = q * (kn2 / 2) + jj;
+        float2 za = make_float2(-b32, -b32), zb = za;
 #pragma unroll
         for (int c = 0; c < F; ++c) {
           const float* xc = xt + (int64_t)c * kN;
@@ -1036,13 +1070,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
           za = __ffma2_rn(make_float2(a32[c], a32[c]), xa, za);  // per lane: fmaf(a_c, x, z)
           zb = __ffma2_rn(make_float2(a32[c], a32[c]), xb, zb);
         }
+        dif_store(j, za, zb);
       }
-      const float2 a0 = cadd(za, zb);
-      float2 wj = twiddle(tw, j >> 1);  // W_32768^j = W_16384^(j/2) (x W_32768 if j odd)
-      if (j & 1) wj = cmul(wj, w32768);
-      const float2 a1 = cmul(csub(za, zb), wj);
-      buf[pad(j)] = q == 0 ? a0 : a1;
-      st_async_f2(rbuf + (uint32_t)pad(j) * 8u, q == 0 ? a1 : a0, rbar_dif);
     }
     // this trace's x is consumed: stream my half of the next one into L2 during C-E
 #if GPOEO_FZ_PREFETCH == 1
@@ -1067,17 +1096,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     // m = (kn2 - k2 - q) mod kn2; q = 0, k2 = 0 pairs bin 0 with the Nyquist bin n.
     constexpr int PPT = kn2 / 2 / kT;  // pairs per thread
     float pa[PPT], pb[PPT];
+    // W_65536^k along k = k0 + 1024 i: one product by W_64 per step (as in phase B)
+    float2 W;
+    {
+      const int k0 = 2 * (int)threadIdx.x + q;
+      W = cmul(twiddle(tw, k0 >> 2), kW65536[k0 & 3]);
+    }
 #pragma unroll
     for (int i = 0; i < PPT; ++i) {
       const int k2 = threadIdx.x + i * kT;  // < kn2 / 2
-      const int k = 2 * k2 + q;
       const int m = (kn2 - k2 - q) & (kn2 - 1);
       const float2 Zk = buf[pad(k2)];
       const float2 Zp = buf[pad(m)];
       const float2 E = cscale(0.5f, __fadd2_rn(Zk, make_float2(Zp.x, -Zp.y)));  // (Z_k + conj Z_p) / 2
       const float2 O = cscale(0.5f, __fadd2_rn(make_float2(Zk.y, -Zk.x), make_float2(Zp.y, Zp.x)));
-      const float2 W = cmul(twiddle(tw, k >> 2), kW65536[k & 3]);
       const float2 T = cmul(W, O);
+      W = cmul(W, make_float2(9.951847266722e-01f, -9.801714032956e-02f));  // x W_65536^1024
       const float2 Xa = cadd(E, T), Xb = csub(E, T);
       pa[i] = Xa.x * Xa.x + Xa.y * Xa.y;
       pb[i] = Xb.x * Xb.x + Xb.y * Xb.y;

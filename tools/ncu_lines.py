@@ -3,7 +3,8 @@
 
     python tools/ncu_lines.py gpurun_out/bucket.ncu-rep score_bucket_kernel [lib.so] [--top 40] [--section I]
 
-(--section I: the I-th "Kernel Name" block of the source page, for reports of several launches)
+(--section I: the I-th "Kernel Name" block of the source page, for reports of several launches;
+ --outer: attribute inlined helpers to the kernel-body line they were called from)
 
 Maps each SASS offset of the kernel to its source line with `nvdisasm -g` on the cubin
 extracted from the library (built with -lineinfo), then sums "Instructions Executed"
@@ -29,14 +30,17 @@ def _op(ins: str) -> str:
     return toks[0] if toks else ""
 
 
-def sass_lines(lib: str, kernel_re: str) -> dict:
+def sass_lines(lib: str, kernel_re: str, outer: bool = False) -> dict:
+    """SASS offset -> (source line, opcode). outer: the kernel-body line an inlined helper was
+    called from (nvdisasm -gi inlining chains), instead of the helper's own line."""
     tmp = tempfile.mkdtemp()
     subprocess.check_call(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, stdout=subprocess.DEVNULL)
     out = {}
     for f in os.listdir(tmp):
         if not f.endswith(".cubin"):
             continue
-        txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, f)], capture_output=True, text=True).stdout
+        txt = subprocess.run(["nvdisasm", "-gi" if outer else "-g", "-c", os.path.join(tmp, f)], capture_output=True,
+                             text=True).stdout
         cur_fn, cur_line = None, None
         for ln in txt.splitlines():
             m = re.match(r"\s*\.text\.(\S+):", ln)
@@ -45,7 +49,9 @@ def sass_lines(lib: str, kernel_re: str) -> dict:
                 continue
             m = re.search(r"//## File \"([^\"]+)\", line (\d+)", ln)
             if m:
-                cur_line = f"{os.path.basename(m.group(1))}:{m.group(2)}"
+                # with -gi a chain "helper line inlined at ..." ends with the outermost line: the last wins
+                if not outer or "inlined at" not in ln:
+                    cur_line = f"{os.path.basename(m.group(1))}:{m.group(2)}"
                 continue
             m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?)\s*;?\s*$", ln)
             if m and cur_fn and re.search(kernel_re, cur_fn):
@@ -70,7 +76,7 @@ def main():
         "Warp Stall Sampling (All Samples)")
     data = [r for r in rows[2:] if len(r) == len(hdr)]
     base = int(data[0][ia], 16)
-    maps = sass_lines(lib, kre)
+    maps = sass_lines(lib, kre, outer="--outer" in sys.argv)
     # pick the function whose size matches the profile best
     isrc = hdr.index("Source")
     best = max(maps.values(), key=lambda m: sum(1 for r in data if m.get(int(r[ia], 16) - base, (0, ""))[1]
