@@ -1187,7 +1187,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(fz::kT, 1)
     // complete_tx on its barrier -- no fence, and no remote read in phase E
     {
       const uint32_t rprx = mapa_u32(smem_u32(Prx), partner), rbar_p = mapa_u32(mb_p, partner);
-      const int n = push_hi - mlo + 1;  // my bins [mlo, push_hi]
+      const int n = push_hi >= mlo ? push_hi - mlo + 1 : 0;  // my bins [mlo, push_hi]
       for (int e = 4 * threadIdx.x; e + 4 <= n; e += 4 * kT)
         st_async_f4(rprx + (uint32_t)e * 4u, *reinterpret_cast<const float4*>(P + mlo + e), rbar_p);
       if ((int)threadIdx.x < (n & 3)) {
