@@ -78,6 +78,15 @@ typedef struct {
   int32_t num_groups;     /* NumG in [1, 8], default 4: GMM groups of Alg.2 l.8 (Z12)       */
   int32_t gmm_max_iters;  /* >= 1, default 32: CEM assignment-pass cap (Z12)                */
   float feature_weights[GPOEO_MAX_FEATURES]; /* w_c of the composite (Z1), default 1     */
+  int32_t bounded_search; /* 1 (default) or 0. Alg. 1 keeps only argmins of Err (l.9-10,
+                             l.18-19), so with 1 a query stops as soon as the
+                             partial sum of its pair errors e_i >= 0 (Alg. 2 l.17-19) proves
+                             Err(L) > the Err of an already scored query of the same trace
+                             and phase (branch and bound; the bound only ever holds an Err
+                             that some query reached, so the argmin -- and every result
+                             field -- is the same as with 0). Such a query's score reads
+                             +inf on the debug surfaces (gpoeo_detail.cand_err,
+                             gpoeo_local_scores). 0: every query is scored to the end.    */
 } gpoeo_params;
 
 /* Per-trace result of Alg. 1. 24 bytes. */
@@ -317,6 +326,7 @@ typedef struct {
   int64_t n_candidate_queries;
   int64_t n_local_queries;
   int64_t cem_sample_passes; /* sum over windows of (CEM passes x L) + final pass over W_{i+1} */
+  int64_t n_pruned_queries;  /* queries the bounded search stopped (bounded_search = 1)      */
 } gpoeo_counters;
 int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t batch, gpoeo_counters* out,
                         void* stream);

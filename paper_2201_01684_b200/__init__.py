@@ -34,12 +34,13 @@ class GpoeoParams(ctypes.Structure):
         ("num_groups", ctypes.c_int32),
         ("gmm_max_iters", ctypes.c_int32),
         ("feature_weights", ctypes.c_float * MAX_FEATURES),
+        ("bounded_search", ctypes.c_int32),
     ]
 
 
 class GpoeoCounters(ctypes.Structure):
     _fields_ = [("n_candidate_queries", ctypes.c_int64), ("n_local_queries", ctypes.c_int64),
-                ("cem_sample_passes", ctypes.c_int64)]
+                ("cem_sample_passes", ctypes.c_int64), ("n_pruned_queries", ctypes.c_int64)]
 
 
 RESULT_DTYPE = np.dtype([("period", "<i4"), ("period_s", "<f4"), ("error", "<f4"), ("status", "<i4"),
@@ -432,7 +433,7 @@ def read_counters(workspace, p: GpoeoParams, batch: int, stream=None) -> dict:
     _check(load().gpoeo_read_counters(ctypes.c_void_p(workspace.data_ptr()), ctypes.byref(p), batch,
                                       ctypes.byref(c), _stream_handle(stream)), "gpoeo_read_counters")
     return dict(n_candidate_queries=c.n_candidate_queries, n_local_queries=c.n_local_queries,
-                cem_sample_passes=c.cem_sample_passes)
+                cem_sample_passes=c.cem_sample_passes, n_pruned_queries=c.n_pruned_queries)
 
 
 def version() -> int:

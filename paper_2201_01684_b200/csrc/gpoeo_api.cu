@@ -56,6 +56,7 @@ int validate(const gpoeo_params* p) {
   if (p->max_candidates < 1 || p->max_candidates > GPOEO_MAX_CANDIDATES) return GPOEO_ERR_INVALID_ARGUMENT;
   if (p->num_groups < 1 || p->num_groups > GPOEO_MAX_GROUPS) return GPOEO_ERR_INVALID_ARGUMENT;
   if (p->gmm_max_iters < 1 || p->gmm_max_iters > 1000000) return GPOEO_ERR_INVALID_ARGUMENT;
+  if (p->bounded_search != 0 && p->bounded_search != 1) return GPOEO_ERR_INVALID_ARGUMENT;
   // N not a power of two: the band-limited DFT holds the band in shared memory
   if (!is_pow2(p->n_samples) && band_smem_bytes(make_plan(p, 0), false) > kBandSmemMax) return GPOEO_ERR_UNSUPPORTED;
   return GPOEO_OK;
@@ -77,6 +78,7 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
   pl.K = p->max_candidates;
   pl.G = p->num_groups;
   pl.maxit = p->gmm_max_iters;
+  pl.bounded = p->bounded_search;
   pl.c_peak = p->c_peak;
   for (int c = 0; c < GPOEO_MAX_FEATURES; ++c) pl.w[c] = p->feature_weights[c];
   pl.Ts = p->sample_interval;
@@ -104,7 +106,7 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
 
 struct Layout {
   size_t off_y, off_status, off_ncand, off_ck, off_cL, off_cP, off_cerr, off_bb, off_llo, off_lhi, off_lbase,
-      off_ia, off_ib, off_xa, off_xb, off_lerr, off_lab, off_ctr, total;
+      off_ia, off_ib, off_xa, off_xb, off_lerr, off_lab, off_ctr, off_bound, total;
   int32_t lab_stride;
 };
 
@@ -129,6 +131,7 @@ Layout layout(const Plan& pl) {
   L.off_llo = take(sizeof(int32_t) * B);
   L.off_lhi = take(sizeof(int32_t) * B);
   L.off_lbase = take(sizeof(int64_t) * B);
+  L.off_bound = take(sizeof(double) * B);
   L.off_ia = take(sizeof(int4) * B * K);
   L.off_ib = take(sizeof(int4) * B * ML);
   // xl arrays (L > kBucketSplitL) only when the band reaches there
@@ -157,6 +160,8 @@ Work carve(const Plan& pl, const Layout& L, void* ws) {
   w.local_lo = reinterpret_cast<int32_t*>(b + L.off_llo);
   w.local_hi = reinterpret_cast<int32_t*>(b + L.off_lhi);
   w.local_base = reinterpret_cast<int64_t*>(b + L.off_lbase);
+  w.bound = reinterpret_cast<double*>(b + L.off_bound);
+  w.rank_ctr = w.ctr + kRankCtrBase;
   w.list_a = ItemList{reinterpret_cast<int4*>(b + L.off_ia), (int64_t)pl.batch * pl.K, &w.ctr[CTR_A_SMALL],
                       &w.ctr[CTR_A_BIG], &w.ctr[CTR_CUR_A_SMALL], &w.ctr[CTR_CUR_A_BIG],
                       reinterpret_cast<int4*>(b + L.off_xa), &w.ctr[CTR_A_XL], &w.ctr[CTR_CUR_A_XL]};
@@ -210,7 +215,7 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
   CK(mark(4));
   if (pl.batch > 0)
     CK(launch_score(pl, w.y, w.list_b, w.local_err, w.lab_scratch, L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmin,
-                    pl.Lmax, s));
+                    pl.Lmax, s, pl.bounded ? w.bound : nullptr, &w.ctr[CTR_PRUNED]));
   CK(mark(5));
   if (pl.batch > 0) CK(launch_final(pl, w, results, detail, s));
   CK(mark(6));
@@ -366,6 +371,7 @@ void gpoeo_default_params(gpoeo_params* p, int32_t n_samples, int32_t n_features
   p->num_groups = 4;
   p->gmm_max_iters = 32;
   for (int c = 0; c < GPOEO_MAX_FEATURES; ++c) p->feature_weights[c] = 1.0f;
+  p->bounded_search = 1;
 }
 
 int gpoeo_validate_params(const gpoeo_params* p) { return validate(p); }
@@ -824,6 +830,7 @@ int gpoeo_read_counters(const void* workspace, const gpoeo_params* p, int64_t ba
   out->n_candidate_queries = (int64_t)(h[CTR_A_SMALL] + h[CTR_A_BIG] + h[CTR_A_XL]);
   out->n_local_queries = (int64_t)(h[CTR_B_SMALL] + h[CTR_B_BIG] + h[CTR_B_XL]);
   out->cem_sample_passes = (int64_t)h[CTR_CEM_PASSES];
+  out->n_pruned_queries = (int64_t)h[CTR_PRUNED];
   return GPOEO_OK;
 }
 

@@ -13,7 +13,14 @@ constexpr int kSubwarpMaxL = 512;    // L <= 512: teams of <= 32 lanes, window i
 constexpr int kLpt = 16;             // samples per lane in register mode
 constexpr int kLabCap = 8192;        // warp mode: labels in smem up to this L, else global scratch
 constexpr int kPeakCap = 1024;       // peaks above threshold held for the rank sort
-constexpr int kCounterSlots = 16;
+// Bounded search (gpoeo_params.bounded_search): a phase's queries are listed in rank order --
+// rank r of every trace before rank r + 1 (local range: distance from L_b, candidates: the
+// spectral ranking) -- so most of a trace's queries start after its better-placed ones have
+// finished and tightened the trace's bound. Ranks >= kRankBuckets - 1 share the last bucket.
+constexpr int kRankBuckets = 32;
+constexpr int kRankCtrBase = 16;  // counter slots [16, 16 + 3 kRankBuckets): per (class, rank) counts;
+                                  // the next 3 kRankBuckets: the scatter cursors
+constexpr int kCounterSlots = kRankCtrBase + 2 * 3 * kRankBuckets;
 constexpr int kMaxScoreCtas = 148 * 4;  // cap of the persistent scorer grid
 
 // Host-derived plan of one call (every trace shares it).
@@ -23,6 +30,7 @@ struct Plan {
   int32_t k_lo, k_hi;         // candidate band of bins (Z21)
   int64_t stride;             // floats between traces
   int32_t Lmin, Lmax, K, G, maxit;
+  int32_t bounded;            // gpoeo_params.bounded_search
   float c_peak;
   float w[GPOEO_MAX_FEATURES];
   double Ts;
@@ -68,6 +76,7 @@ enum CounterSlot {
   CTR_B_XL = 11,       // local queries with L > kBucketSplitL
   CTR_CUR_A_XL = 12,
   CTR_CUR_B_XL = 13,
+  CTR_PRUNED = 14,     // queries stopped by the bound (bounded search)
 };
 
 #ifndef GPOEO_BUCKET_MIN_L
@@ -115,6 +124,17 @@ __device__ __forceinline__ void append_items(const ItemList& l, int t, int L0, i
   }
 }
 
+// kernel class of a query: 0 team (L < kBucketMinL), 1 mid bucketed, 2 xl
+__device__ __forceinline__ int query_class(int32_t L) {
+  return L < kBucketMinL ? 0 : (L <= kBucketSplitL ? 1 : 2);
+}
+// item at position pos of its class's section
+__device__ __forceinline__ void list_put(const ItemList& l, int cls, unsigned long long pos, int4 item) {
+  if (cls == 0) l.items[pos] = item;
+  else if (cls == 1) l.items[l.cap - 1 - (int64_t)pos] = item;
+  else l.xl[pos] = item;
+}
+
 __device__ __forceinline__ void append_item(const ItemList& l, int t, int L, int slot) {
   if (L < kBucketMinL) {
     l.items[atomicAdd(l.n_small, 1ull)] = make_int4(t, L, slot, 0);
@@ -138,6 +158,8 @@ struct Work {
   int32_t* local_lo;        // [B]
   int32_t* local_hi;        // [B]
   int64_t* local_base;      // [B]
+  double* bound;            // [B] bounded search: the smallest Err a finished query of the trace reached
+  unsigned long long* rank_ctr;  // [2][3][kRankBuckets] rank-ordered list construction (in ctr)
   ItemList list_a;          // [B*K]   candidate queries (trace, L, out slot, -)
   ItemList list_b;          // [B*max_local] local queries
   double* local_err;        // [B*max_local]
@@ -161,8 +183,12 @@ cudaError_t launch_spectrum_band(const Plan& p, const float* y, const int32_t* s
 // y_out may be null (spectral-only: nothing but the results leaves the chip).
 cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* y_out, float* spectra,
                                   int mode, cudaStream_t s);
+// bound: null, or per-trace upper bounds on the winning Err of the list's queries (bounded
+// search: a query stops when its partial pair-error sum proves Err(L) > bound[t], writes
+// +inf and bumps *pruned_ctr; a finished query lowers bound[t] to its Err by atomicMin).
 cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
-                         int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s);
+                         int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s,
+                         double* bound = nullptr, unsigned long long* pruned_ctr = nullptr);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);
 cudaError_t launch_local_scores(const Plan& p, Work w, double* out, cudaStream_t s);
 

@@ -1165,7 +1165,32 @@ struct ScoreArgs {
   int32_t lab_stride;
   int32_t bucket_lcap;   // bucket path handles kBucketMinL <= L <= bucket_lcap
   unsigned long long* cem_ctr;
+  double* bound;         // bounded search: per-trace upper bound on the winning Err (null: off)
+  unsigned long long* pruned;  // queries stopped by the bound
 };
+
+// Bounded search. Alg. 1 only needs the argmin of Err (l.9-10, l.18-19). Err(L) = (sum_i e_i)
+// / npairs with every e_i >= 0 (Alg. 2 l.17-19: a count-weighted mean of SMAPEs), and fp64
+// addition of non-negative terms is monotone, so a partial sum acc already gives
+// Err(L) >= acc / npairs. If acc > bound * npairs * (1 + 1e-12) -- bound being an Err some
+// query of the trace reached, hence >= the winner's -- then Err(L) > the winner's Err
+// strictly (the factor covers the rounding of the product and of the final division), L
+// cannot be the argmin (ties go to the smaller L only between equal Err), and the query
+// stops. The winner itself is never stopped: its partial sums stay <= its Err * npairs.
+__device__ __forceinline__ double bound_scale(int32_t npairs) { return (double)npairs * (1.0 + 1e-12); }
+
+// Err(L) (or +inf for a stopped query) into the query's slot; a finished query lowers its
+// trace's bound (Err >= +0: the bit patterns of non-negative doubles order like the values).
+__device__ __forceinline__ void write_err(const ScoreArgs& a, int4 q, bool pruned, double sum, int32_t npairs) {
+  if (pruned) {
+    a.err_out[q.z] = INFINITY;
+    atomicAdd(a.pruned, 1ull);
+    return;
+  }
+  const double err = sum / (double)npairs;
+  a.err_out[q.z] = err;
+  if (a.bound) atomicMin(reinterpret_cast<unsigned long long*>(a.bound + q.x), (unsigned long long)__double_as_longlong(err));
+}
 
 __device__ __forceinline__ int4 fetch_item(const ScoreArgs& a, int64_t k) {
   return a.items[a.reverse ? a.cap - 1 - k : k];
@@ -1178,6 +1203,8 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
   __shared__ double s_team[kScoreThreads];
   __shared__ double s_red[2 * kWarps * 32];
   __shared__ double s_ys[kLpt * kScoreThreads];  // samples, [u][thread]
+  __shared__ double s_part[2][kWarps];            // bounded search: per-warp partial sums
+  __shared__ double s_bnd[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long total = *a.count;
   long long passes = 0;
@@ -1202,13 +1229,38 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
     const int lt = tid & (tau - 1);
     // warp-uniform trip count (sub-warp teams of one warp: team0 .. team0 + 32/tau - 1)
     const int team0 = tau >= 32 ? team : (warp * 32) / tau;
-    const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
-    for (int i = 0; i < trips; ++i) {
-      const int pidx = team + i * nteams;
-      const bool has = pidx < npairs;
-      const float* A = yt + (int64_t)(has ? pidx : 0) * L;
-      const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
-      if (has) acc += e;
+    bool pruned = false;
+    if (a.bound) {
+      // bounded: CTA-uniform trips; after each, the teams' partial sums (fixed order) against
+      // the trace's current bound (one barrier per trip, double-buffered)
+      const int trips = (npairs + nteams - 1) / nteams;
+      const double scale = bound_scale(npairs);
+      for (int i = 0; i < trips; ++i) {
+        const int pidx = team + i * nteams;
+        const bool has = pidx < npairs;
+        const float* A = yt + (int64_t)(has ? pidx : 0) * L;
+        const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
+        if (has) acc += e;
+        double part = lt == 0 ? acc : 0.0;
+#pragma unroll
+        for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(FULL, part, off);
+        if (lane == 0) s_part[i & 1][warp] = part;
+        if (tid == 0) s_bnd[i & 1] = __ldcg(a.bound + t);
+        __syncthreads();
+        double tot = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) tot += s_part[i & 1][w];
+        if (tot > s_bnd[i & 1] * scale) { pruned = true; break; }  // CTA-uniform
+      }
+    } else {
+      const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
+      for (int i = 0; i < trips; ++i) {
+        const int pidx = team + i * nteams;
+        const bool has = pidx < npairs;
+        const float* A = yt + (int64_t)(has ? pidx : 0) * L;
+        const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
+        if (has) acc += e;
+      }
     }
     if (lt != 0) acc = 0.0;
     // per-team partials -> Err(L): fixed-shape tree (xor butterfly per warp, then warps in
@@ -1221,7 +1273,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
       double sum = 0.0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) sum += s_team[w];
-      a.err_out[q.z] = sum / (double)npairs;
+      write_err(a, q, pruned, sum, npairs);
     }
     __syncthreads();
   }
@@ -1251,6 +1303,17 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
     const int32_t npairs = (a.row_n ? a.row_n[t] : a.N) / L - 1;
     const float* yt = a.y + t * a.ystride;
     double acc = 0.0;
+    bool pruned = false;
+    const double scale = bound_scale(npairs);
+    // bounded search: acc is warp-uniform (xor-butterfly sums are identical in every lane);
+    // lane 0 reads the trace's current bound after each pair
+    auto stop = [&]() -> bool {
+      if (!a.bound) return false;
+      double b = 0.0;
+      if (lane == 0) b = __ldcg(a.bound + t);
+      b = __shfl_sync(FULL, b, 0);
+      return acc > b * scale;
+    };
     if (L <= a.bucket_lcap) {
       BucketView bv =
           BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap, VS), a.bucket_lcap, VS);
@@ -1259,20 +1322,23 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
         // kBucketWarps == 1: pairs in order, so the previous final pass saw this W_i
         acc += pair_err_bucket<G, VS>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes, pidx != warp, range);
         __syncwarp();
+        if (stop()) { pruned = true; break; }
       }
     } else {
       uint8_t* lab = a.lab_scratch + ((int64_t)blockIdx.x * kBucketWarps + warp) * a.lab_stride;
       for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
         acc += pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
         __syncwarp();
+        if (stop()) { pruned = true; break; }
       }
     }
+    static_assert(kBucketWarps == 1, "the bounded-search stop is warp-uniform, not CTA-uniform");
     if (lane == 0) s_team[warp] = acc;
     __syncthreads();
     if (tid == 0) {
       double sum = 0.0;
       for (int w = 0; w < kBucketWarps; ++w) sum += s_team[w];
-      a.err_out[q.z] = sum / (double)npairs;
+      write_err(a, q, pruned, sum, npairs);
     }
     __syncthreads();
   }
@@ -1382,8 +1448,12 @@ static cudaError_t launch_forked(const ScoreArgs& a, const ItemList& list, int32
 }
 
 cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
-                         int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s) {
+                         int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s,
+                         double* bound, unsigned long long* pruned_ctr) {
+  if (bound && !pruned_ctr) return cudaErrorInvalidValue;
   ScoreArgs a{};
+  a.bound = bound;
+  a.pruned = pruned_ctr;
   a.y = y;
   a.N = p.N;
   a.row_n = p.row_n;

@@ -12,6 +12,14 @@
 
 namespace gpoeo {
 
+// rank of a local query: distance from L_b, the smaller side first (L_b - 1, L_b + 1,
+// L_b - 2, ...); L_b itself is a candidate (memoised)
+__device__ __forceinline__ int local_rank(int32_t L, int32_t Lb) {
+  const int d = L - Lb;
+  const int r = d < 0 ? -2 * d - 2 : 2 * d - 1;
+  return r < kRankBuckets - 1 ? r : kRankBuckets - 1;
+}
+
 // One thread per trace: argmin (Err, L) over candidates, local range, work-list append.
 __global__ void select_kernel(Plan pc, Work w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -38,20 +46,60 @@ __global__ void select_kernel(Plan pc, Work w) {
   w.local_lo[t] = (int32_t)lo;
   w.local_hi[t] = (int32_t)hi;
   w.local_base[t] = (int64_t)base;
+  // bounded search: the best candidate's Err bounds the winner of the local range from above
+  // (L_b is in the range); finished local queries lower it
+  w.bound[t] = w.cand_err[t * p.K + best];
   // Alg. 2 on every L of the range, except candidates already scored in phase a4: their
   // Err(L) is the same deterministic value (same kernel class for the same L), so it is
-  // copied (the oracle memoises identically).
-  int64_t run0 = lo;
-  for (int64_t L = lo; L <= hi + 1; ++L) {
+  // copied (the oracle memoises identically). The queries are counted per (kernel class,
+  // rank) here and listed in rank order by local_scatter_kernel.
+  const int32_t Lb = (int32_t)(N / kb);
+  for (int64_t L = lo; L <= hi; ++L) {
     int c = -1;
-    if (L <= hi)
-      for (int q = 0; q < nc; ++q)
-        if (w.cand_L[t * p.K + q] == (int32_t)L) c = q;
-    if (c >= 0 || L > hi) {
-      if (L > run0) append_items(w.list_b, (int)t, (int)run0, (int)(L - run0), (int)(base + (run0 - lo)));
-      if (c >= 0) w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
-      run0 = L + 1;
+    for (int q = 0; q < nc; ++q)
+      if (w.cand_L[t * p.K + q] == (int32_t)L) c = q;
+    if (c >= 0) {
+      w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
+    } else {
+      atomicAdd(&w.rank_ctr[query_class((int32_t)L) * kRankBuckets + local_rank((int32_t)L, Lb)], 1ull);
     }
+  }
+}
+
+// One warp per kernel class: exclusive scan of the per-rank counts -> the scatter cursors
+// and the class's list length.
+__global__ void rank_scan_kernel(Work w, ItemList list) {
+  const int cls = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  static_assert(kRankBuckets == 32, "one lane per rank bucket");
+  const unsigned long long n = w.rank_ctr[cls * kRankBuckets + lane];
+  unsigned long long incl = n;
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+  w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + lane] = incl - n;
+  if (lane == 31) *(cls == 0 ? list.n_small : cls == 1 ? list.n_big : list.n_xl) = incl;
+}
+
+// One thread per trace: the local queries of select_kernel, each at the next free position
+// of its (class, rank) section of the list.
+__global__ void local_scatter_kernel(Plan pc, Work w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= pc.batch) return;
+  const Plan p = row_plan(pc, t);
+  if (w.status[t] != GPOEO_TRACE_OK) return;
+  const int nc = w.n_cand[t];
+  const int32_t lo = w.local_lo[t], hi = w.local_hi[t];
+  const int64_t base = w.local_base[t];
+  const int32_t Lb = p.N / w.best_bin[t];
+  for (int32_t L = lo; L <= hi; ++L) {
+    bool memo = false;
+    for (int q = 0; q < nc; ++q) memo |= w.cand_L[t * p.K + q] == L;
+    if (memo) continue;
+    const int cls = query_class(L);
+    const unsigned long long pos =
+        atomicAdd(&w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + local_rank(L, Lb)], 1ull);
+    list_put(w.list_b, cls, pos, make_int4((int)t, L, (int)(base + (L - lo)), 0));
   }
 }
 
@@ -124,7 +172,10 @@ cudaError_t launch_local_scores(const Plan& p, Work w, double* out, cudaStream_t
 
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
-  select_kernel<<<(unsigned)((p.batch + 127) / 128), 128, 0, s>>>(p, w);
+  const unsigned g = (unsigned)((p.batch + 127) / 128);
+  select_kernel<<<g, 128, 0, s>>>(p, w);
+  rank_scan_kernel<<<1, 3 * 32, 0, s>>>(w, w.list_b);
+  local_scatter_kernel<<<g, 128, 0, s>>>(p, w);
   return cudaGetLastError();
 }
 

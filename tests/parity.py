@@ -15,6 +15,8 @@ the GPU's outcome is checked for validity against the oracle itself:
     list (oracle.detect(given_k=...));
   * a single Alg. 2 score off by more than the tolerance: the oracle's CEM decision margin of
     that query must be < THR_CEM (a partition flip at rounding level);
+  * a query the bounded search stopped (score +inf): that L must not be the oracle's argmin
+    (unless another L ties it within THR_ERR);
   * a different Tcand_opt or final L: the oracle's Err of the GPU's choice must be within THR_ERR
     (relative) of its best, or one of the two scores involved must be a flipped query; a
     different Tcand_opt is then followed by the oracle forced to the GPU's bin
@@ -44,12 +46,14 @@ class Tally:
         self.n = 0
         self.exact = 0
         self.reasons: dict[str, int] = {}
+        self.stopped = 0  # Alg. 2 queries the bounded search stopped (score +inf), each checked
 
     def note(self, reason: str):
         self.reasons[reason] = self.reasons.get(reason, 0) + 1
 
     def summary(self) -> str:
-        return f"[parity {self.label}] traces={self.n} exact={self.exact} justified-exclusions={self.reasons}"
+        return (f"[parity {self.label}] traces={self.n} exact={self.exact} justified-exclusions={self.reasons} "
+                f"stopped-queries={self.stopped}")
 
 
 def _p3(y, k: int):
@@ -137,7 +141,19 @@ def check_trace(x, op: O.Params, r, q, gl, d: O.Detection, tally: Tally, where="
     if gl is not None:
         n_loc = ref.local_hi - ref.local_lo + 1
         assert np.isnan(gl[n_loc:]).all(), tag
+        io = ref.period - ref.local_lo
         for i in range(n_loc):
+            if np.isposinf(gl[i]):
+                # bounded search stopped this L: the GPU proved Err(L) > an Err another L of the
+                # trace reached, so L is not the argmin -- on the oracle's scores it must not be
+                # either (up to a near-tie, Z27)
+                if i == io:
+                    others = [e for j, e in enumerate(ref.local_err) if j != i]
+                    ok = bool(others) and _rel_gap(min(others), ref.error) < O.THR_ERR
+                    assert ok, (tag, "stopped L is the oracle's argmin", ref.local_lo + i, ref.local_err[i])
+                    excluded.append("err-tie:stopped")
+                tally.stopped += 1
+                continue
             if not _close(gl[i], ref.local_err[i]):
                 assert ref.local_margin[i] < O.THR_CEM, (tag, "local score", ref.local_lo + i, gl[i], ref.local_err[i],
                                                          ref.local_margin[i])

@@ -50,7 +50,8 @@ def test_default_params_and_struct_layout():
     assert p.min_period == 2 and p.max_period == 512
     assert abs(p.c_peak - 0.65) < 1e-7 and p.max_candidates == 16 and p.num_groups == 4
     assert p.gmm_max_iters == 32 and list(p.feature_weights) == [1.0] * 8
-    assert ctypes.sizeof(g.GpoeoParams) == 80
+    assert p.bounded_search == 1
+    assert ctypes.sizeof(g.GpoeoParams) == 88  # 80 + bounded_search, padded to 8
     assert g.validate(p) == 0
 
 
@@ -60,6 +61,7 @@ def test_default_params_and_struct_layout():
     ("min_period", 1, -1), ("max_period", 513, -1), ("c_peak", 0.0, -1), ("c_peak", 1.5, -1),
     ("max_candidates", 0, -1), ("max_candidates", 33, -1), ("num_groups", 0, -1), ("num_groups", 9, -1),
     ("gmm_max_iters", 0, -1), ("sample_interval", 0.0, -1), ("trace_stride", 3074, -4),
+    ("bounded_search", 2, -1), ("bounded_search", -1, -1),
 ])
 def test_validation_codes(field, value, code):
     p = g.default_params(1024, 3)

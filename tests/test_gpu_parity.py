@@ -261,7 +261,9 @@ def test_parameter_variants(kw):
 def test_deterministic_and_batch_order_invariant():
     spec = tg.CFG2.with_(batch=24)
     x = tg.generate_host(spec)
-    p = g.params_for(spec)
+    # every score to the end: the debug surfaces are bit-reproducible too (with the bounded
+    # search only the results are -- which queries stop depends on timing)
+    p = g.params_for(spec, bounded_search=0)
     r1, d1, l1, _ = _detect(x, p)
     r2, d2, l2, _ = _detect(x, p)
     assert r1.tobytes() == r2.tobytes() and d1.tobytes() == d2.tobytes() and l1.tobytes() == l2.tobytes()
@@ -269,6 +271,33 @@ def test_deterministic_and_batch_order_invariant():
     r3, d3, l3, _ = _detect(x[perm], p)
     assert r3.tobytes() == r1[perm].tobytes() and d3.tobytes() == d1[perm].tobytes()
     assert l3.tobytes() == l1[perm].tobytes()
+
+
+@pytest.mark.parametrize("spec,some_stop", [(tg.CFG2, True), (tg.CFG3.with_(batch=48), True),
+                                            (tg.CFG5.with_(batch=4), False)])
+def test_bounded_search_same_results(spec, some_stop):
+    """Bounded search (gpoeo_params.bounded_search = 1, the default) against every query scored
+    to the end, both on the GPU: identical result records and best_err, identical scores where
+    a query finished, and every stopped query's full score strictly above its trace's winner
+    (what the stop proved)."""
+    x = tg.generate_host(spec)
+    B = x.shape[0]
+    r0, d0, l0, _ = _detect(x, g.params_for(spec, bounded_search=0))
+    stopped = 0
+    for rep in range(2):
+        r1, d1, l1, ws = _detect(x, g.params_for(spec))
+        assert r1.tobytes() == r0.tobytes(), rep
+        assert d1["best_err"].tobytes() == d0["best_err"].tobytes()
+        assert d1["cand_err"].tobytes() == d0["cand_err"].tobytes()
+        fin = np.isfinite(l1) | np.isnan(l1)
+        assert l1[fin].tobytes() == l0[fin].tobytes()
+        inf = np.isposinf(l1)
+        assert (l0[inf] > np.repeat(d0["best_err"][:, None], l0.shape[1], 1)[inf]).all()
+        c = g.read_counters(ws, g.params_for(spec), B)
+        assert c["n_pruned_queries"] == int(inf.sum())
+        stopped += int(inf.sum())
+    print(f"[bounded {spec.name}] stopped {stopped / 2:.0f} of {int(np.isfinite(l0).sum())} local scores per call")
+    assert stopped > 0 or not some_stop  # 4 traces: every query starts before any finishes
 
 
 def test_host_entry_point_matches_device():
@@ -295,6 +324,7 @@ def test_work_counters():
         want += sum(1 for L in range(det["local_lo"][i], det["local_hi"][i] + 1) if L not in cands)
     assert c["n_local_queries"] == want
     assert c["cem_sample_passes"] > 0
+    assert 0 <= c["n_pruned_queries"] <= c["n_local_queries"]
 
 
 @pytest.mark.slow

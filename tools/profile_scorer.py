@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--first", type=int, default=0)
     ap.add_argument("--maxit", type=int, default=32, help="CEM pass cap (timing experiments only)")
+    ap.add_argument("--bounded", type=int, default=1, help="gpoeo_params.bounded_search")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -34,6 +35,7 @@ def main():
     spec = tg.CFG3.with_(batch=args.batch)
     p = g.params_for(spec)
     p.gmm_max_iters = args.maxit
+    p.bounded_search = args.bounded
     x = torch.empty((args.batch, spec.n_features * spec.n_samples), dtype=torch.float32, device="cuda")
     tg.generate_device(spec, x, first=args.first, count=args.batch)
     ws = g.alloc_workspace(g.workspace_size(p, args.batch))
