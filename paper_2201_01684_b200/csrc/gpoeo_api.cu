@@ -206,10 +206,11 @@ int run_detect(const float* traces, const Plan& pl, const Layout& L, void* ws, g
     else if (!pl.row_n && is_pow2(pl.N)) CK(launch_spectrum(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
     else CK(launch_spectrum_band(pl, w.y, w.status, w, nullptr, kPeaksCandidates, s));
   }
+  if (pl.batch > 0) CK(launch_candidate_list(pl, w, s));
   CK(mark(2));
   if (pl.batch > 0)
     CK(launch_score(pl, w.y, w.list_a, w.cand_err, w.lab_scratch, L.lab_stride, &w.ctr[CTR_CEM_PASSES], pl.Lmin,
-                    pl.Lmax, s));
+                    pl.Lmax, s, pl.bounded ? w.bound : nullptr, &w.ctr[CTR_PRUNED]));
   CK(mark(3));
   if (pl.batch > 0) CK(launch_select(pl, w, s));
   CK(mark(4));

@@ -18,9 +18,10 @@ constexpr int kPeakCap = 1024;       // peaks above threshold held for the rank 
 // spectral ranking) -- so most of a trace's queries start after its better-placed ones have
 // finished and tightened the trace's bound. Ranks >= kRankBuckets - 1 share the last bucket.
 constexpr int kRankBuckets = 32;
-constexpr int kRankCtrBase = 16;  // counter slots [16, 16 + 3 kRankBuckets): per (class, rank) counts;
-                                  // the next 3 kRankBuckets: the scatter cursors
-constexpr int kCounterSlots = kRankCtrBase + 2 * 3 * kRankBuckets;
+constexpr int kRankCtrBase = 16;  // counter slots from 16: per phase (candidates, local) 3 kRankBuckets
+                                  // per-(class, rank) counts, then 3 kRankBuckets scatter cursors
+constexpr int kRankCtrPhase = 2 * 3 * kRankBuckets;
+constexpr int kCounterSlots = kRankCtrBase + 2 * kRankCtrPhase;
 constexpr int kMaxScoreCtas = 148 * 4;  // cap of the persistent scorer grid
 
 // Host-derived plan of one call (every trace shares it).
@@ -159,7 +160,7 @@ struct Work {
   int32_t* local_hi;        // [B]
   int64_t* local_base;      // [B]
   double* bound;            // [B] bounded search: the smallest Err a finished query of the trace reached
-  unsigned long long* rank_ctr;  // [2][3][kRankBuckets] rank-ordered list construction (in ctr)
+  unsigned long long* rank_ctr;  // [2 phases][2][3][kRankBuckets] rank-ordered list construction (in ctr)
   ItemList list_a;          // [B*K]   candidate queries (trace, L, out slot, -)
   ItemList list_b;          // [B*max_local] local queries
   double* local_err;        // [B*max_local]
@@ -189,6 +190,8 @@ cudaError_t launch_spectral_fused(const Plan& p, const float* x, Work w, float* 
 cudaError_t launch_score(const Plan& p, const float* y, const ItemList& list, double* err_out, uint8_t* lab_scratch,
                          int32_t lab_stride, unsigned long long* cem_ctr, int32_t min_L, int32_t max_L, cudaStream_t s,
                          double* bound = nullptr, unsigned long long* pruned_ctr = nullptr);
+// The candidate queries (counted per (class, rank) by the spectral kernels) in rank order.
+cudaError_t launch_candidate_list(const Plan& p, Work w, cudaStream_t s);
 cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s);
 cudaError_t launch_local_scores(const Plan& p, Work w, double* out, cudaStream_t s);
 

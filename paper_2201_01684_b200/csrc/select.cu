@@ -61,24 +61,47 @@ __global__ void select_kernel(Plan pc, Work w) {
     if (c >= 0) {
       w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
     } else {
-      atomicAdd(&w.rank_ctr[query_class((int32_t)L) * kRankBuckets + local_rank((int32_t)L, Lb)], 1ull);
+      atomicAdd(&w.rank_ctr[kRankCtrPhase + query_class((int32_t)L) * kRankBuckets + local_rank((int32_t)L, Lb)], 1ull);
     }
   }
 }
 
 // One warp per kernel class: exclusive scan of the per-rank counts -> the scatter cursors
 // and the class's list length.
-__global__ void rank_scan_kernel(Work w, ItemList list) {
+__global__ void rank_scan_kernel(unsigned long long* ctr, ItemList list) {
   const int cls = threadIdx.x >> 5, lane = threadIdx.x & 31;
   static_assert(kRankBuckets == 32, "one lane per rank bucket");
-  const unsigned long long n = w.rank_ctr[cls * kRankBuckets + lane];
+  const unsigned long long n = ctr[cls * kRankBuckets + lane];
   unsigned long long incl = n;
   for (int off = 1; off < 32; off <<= 1) {
     const unsigned long long o = __shfl_up_sync(0xffffffffu, incl, off);
     if (lane >= off) incl += o;
   }
-  w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + lane] = incl - n;
+  ctr[3 * kRankBuckets + cls * kRankBuckets + lane] = incl - n;
   if (lane == 31) *(cls == 0 ? list.n_small : cls == 1 ? list.n_big : list.n_xl) = incl;
+}
+
+// One thread per trace: candidate c (spectral rank c, Alg. 1 l.4) at the next free position of
+// its (class, rank c) section of list_a, so the strongest peaks' queries run first.
+__global__ void cand_scatter_kernel(Plan pc, Work w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= pc.batch) return;
+  if (w.status[t] != GPOEO_TRACE_OK) return;
+  const int nc = w.n_cand[t];
+  for (int c = 0; c < nc; ++c) {
+    const int32_t L = w.cand_L[t * pc.K + c];
+    const int cls = query_class(L);
+    const unsigned long long pos = atomicAdd(&w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + c], 1ull);
+    list_put(w.list_a, cls, pos, make_int4((int)t, L, (int)(t * pc.K + c), 0));
+  }
+}
+
+cudaError_t launch_candidate_list(const Plan& p, Work w, cudaStream_t s) {
+  if (p.batch == 0) return cudaSuccess;
+  static_assert(GPOEO_MAX_CANDIDATES <= kRankBuckets, "a rank bucket per candidate rank");
+  rank_scan_kernel<<<1, 3 * 32, 0, s>>>(w.rank_ctr, w.list_a);
+  cand_scatter_kernel<<<(unsigned)((p.batch + 127) / 128), 128, 0, s>>>(p, w);
+  return cudaGetLastError();
 }
 
 // One thread per trace: the local queries of select_kernel, each at the next free position
@@ -98,7 +121,7 @@ __global__ void local_scatter_kernel(Plan pc, Work w) {
     if (memo) continue;
     const int cls = query_class(L);
     const unsigned long long pos =
-        atomicAdd(&w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + local_rank(L, Lb)], 1ull);
+        atomicAdd(&w.rank_ctr[kRankCtrPhase + 3 * kRankBuckets + cls * kRankBuckets + local_rank(L, Lb)], 1ull);
     list_put(w.list_b, cls, pos, make_int4((int)t, L, (int)(base + (L - lo)), 0));
   }
 }
@@ -174,7 +197,7 @@ cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
   const unsigned g = (unsigned)((p.batch + 127) / 128);
   select_kernel<<<g, 128, 0, s>>>(p, w);
-  rank_scan_kernel<<<1, 3 * 32, 0, s>>>(w, w.list_b);
+  rank_scan_kernel<<<1, 3 * 32, 0, s>>>(w.rank_ctr + kRankCtrPhase, w.list_b);
   local_scatter_kernel<<<g, 128, 0, s>>>(p, w);
   return cudaGetLastError();
 }

@@ -14,7 +14,7 @@
 // After the FFT the CTA overwrites its Z buffer with its share of P (fp32); CTA rank 0
 // then finds the in-band peaks (Z5: P[k] > P[k-1] and P[k] >= P[k+1], mirrored edges),
 // keeps the top K by (P desc, k asc) (Z8), thresholds P > c_peak^2 P_max (Z3, Z7),
-// maps k -> floor(N/k) (Z9) and deduplicates, appending one Alg.2 query per candidate.
+// maps k -> floor(N/k) (Z9) and deduplicates, counting one Alg.2 query per candidate.
 #include <cooperative_groups.h>
 
 #include "gpoeo_internal.cuh"
@@ -166,7 +166,7 @@ struct PView {
 // Rows a3, second half: given the in-band peak maximum pmax (< 0: no peak) and the peaks
 // above c_peak^2 pmax collected in ps (ps.count of them, the first kPeakCap stored), keep
 // the top K by (P desc, k asc), map k -> floor(N/k) and dedupe (Alg.1 l.3-5, P:311-314;
-// Z5, Z7-Z9); append one Alg. 2 query per candidate and write the trace status. Called
+// Z5, Z7-Z9); count one Alg. 2 query per candidate and write the trace status. Called
 // by the whole CTA (T threads) that owns ps; Pv sees the whole spectrum.
 template <class PV, int T>
 __device__ void finish_candidates(const Plan& p, const PV& Pv, int64_t t, int32_t st, Work& w, PeakShared& ps,
@@ -263,8 +263,10 @@ __device__ void finish_candidates(const Plan& p, const PV& Pv, int64_t t, int32_
     if (status == GPOEO_TRACE_OK && p.k_lo > p.k_hi) status = GPOEO_TRACE_INSUFFICIENT;  // empty band (Z21)
     if (status == GPOEO_TRACE_OK && nc == 0) status = GPOEO_TRACE_APERIODIC;
     w.status[t] = status;
-    if (status == GPOEO_TRACE_OK) {
-      for (int c2 = 0; c2 < nc; ++c2) append_item(w.list_a, (int)t, w.cand_L[t * p.K + c2], (int)(t * p.K + c2));
+    w.bound[t] = INFINITY;  // bounded search: no candidate scored yet
+    if (status == GPOEO_TRACE_OK) {  // queries listed in rank order by launch_candidate_list
+      for (int c2 = 0; c2 < nc; ++c2)
+        atomicAdd(&w.rank_ctr[query_class(w.cand_L[t * p.K + c2]) * kRankBuckets + c2], 1ull);
     }
   }
 }

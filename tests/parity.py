@@ -15,8 +15,8 @@ the GPU's outcome is checked for validity against the oracle itself:
     list (oracle.detect(given_k=...));
   * a single Alg. 2 score off by more than the tolerance: the oracle's CEM decision margin of
     that query must be < THR_CEM (a partition flip at rounding level);
-  * a query the bounded search stopped (score +inf): that L must not be the oracle's argmin
-    (unless another L ties it within THR_ERR);
+  * a query the bounded search stopped (score +inf): that candidate / L must not be the oracle's
+    argmin (unless another one ties it within THR_ERR);
   * a different Tcand_opt or final L: the oracle's Err of the GPU's choice must be within THR_ERR
     (relative) of its best, or one of the two scores involved must be a flipped query; a
     different Tcand_opt is then followed by the oracle forced to the GPU's bin
@@ -120,7 +120,17 @@ def check_trace(x, op: O.Params, r, q, gl, d: O.Detection, tally: Tally, where="
     assert [int(v) for v in q["cand_L"][:nc]] == ref.cand_L, tag
     # Alg. 2 on every candidate
     flipped_c = set()
+    ib = ref.cand_k.index(ref.best_bin)
     for c in range(nc):
+        if np.isposinf(q["cand_err"][c]):
+            # bounded search stopped this candidate: not the oracle's best either (up to a near-tie)
+            if c == ib:
+                others = [e for j, e in enumerate(ref.cand_err) if j != c]
+                ok = bool(others) and _rel_gap(min(others), ref.cand_err[c]) < O.THR_ERR
+                assert ok, (tag, "stopped candidate is the oracle's best", c, ref.cand_err)
+                excluded.append("err-tie:stopped-candidate")
+            tally.stopped += 1
+            continue
         if not _close(q["cand_err"][c], ref.cand_err[c]):
             assert ref.cand_margin[c] < O.THR_CEM, (tag, "candidate score", c, q["cand_err"][c], ref.cand_err[c],
                                                     ref.cand_margin[c])

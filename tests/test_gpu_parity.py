@@ -288,15 +288,25 @@ def test_bounded_search_same_results(spec, some_stop):
         r1, d1, l1, ws = _detect(x, g.params_for(spec))
         assert r1.tobytes() == r0.tobytes(), rep
         assert d1["best_err"].tobytes() == d0["best_err"].tobytes()
-        assert d1["cand_err"].tobytes() == d0["cand_err"].tobytes()
+        c0, c1 = d0["cand_err"], d1["cand_err"]
+        cinf = np.isposinf(c1)
+        assert c1[~cinf].tobytes() == c0[~cinf].tobytes()
+        best_c = np.array([row[:n].min() if n else 0.0 for row, n in zip(c0, d0["n_candidates"])])
+        assert (c0[cinf] > np.repeat(best_c[:, None], c0.shape[1], 1)[cinf]).all()
         fin = np.isfinite(l1) | np.isnan(l1)
-        assert l1[fin].tobytes() == l0[fin].tobytes()
+        # a stopped candidate inside the local range is copied there as +inf (memoised)
+        same = fin & np.isfinite(l0)
+        assert l1[same].tobytes() == l0[same].tobytes()
         inf = np.isposinf(l1)
         assert (l0[inf] > np.repeat(d0["best_err"][:, None], l0.shape[1], 1)[inf]).all()
         c = g.read_counters(ws, g.params_for(spec), B)
-        assert c["n_pruned_queries"] == int(inf.sum())
-        stopped += int(inf.sum())
-    print(f"[bounded {spec.name}] stopped {stopped / 2:.0f} of {int(np.isfinite(l0).sum())} local scores per call")
+        # stopped queries: candidates + local ones (a memoised copy is not a query)
+        n_memo_inf = sum(int(np.isin(d1["cand_L"][i][:d1["n_candidates"][i]][cinf[i][:d1["n_candidates"][i]]],
+                                     np.arange(d1["local_lo"][i], d1["local_hi"][i] + 1)).sum())
+                         for i in range(B) if r1["status"][i] == 0)
+        assert c["n_pruned_queries"] == int(cinf.sum()) + int(inf.sum()) - n_memo_inf
+        stopped += int(inf.sum()) + int(cinf.sum())
+    print(f"[bounded {spec.name}] stopped {stopped / 2:.0f} of {int(np.isfinite(l0).sum())} local + candidate scores per call")
     assert stopped > 0 or not some_stop  # 4 traces: every query starts before any finishes
 
 
@@ -324,7 +334,7 @@ def test_work_counters():
         want += sum(1 for L in range(det["local_lo"][i], det["local_hi"][i] + 1) if L not in cands)
     assert c["n_local_queries"] == want
     assert c["cem_sample_passes"] > 0
-    assert 0 <= c["n_pruned_queries"] <= c["n_local_queries"]
+    assert 0 <= c["n_pruned_queries"] <= c["n_local_queries"] + c["n_candidate_queries"]
 
 
 @pytest.mark.slow
