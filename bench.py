@@ -366,6 +366,11 @@ def run_gpu(args) -> None:
                      "achieved": achieved_dp / 1e12, "peak": peak_dp / 1e12, "unit": "TDPinstr/s",
                      "frac": achieved_dp / peak_dp, "traffic": traffic, "traffic_note": traffic_note,
                      "work": f"{passes} CEM sample-passes/call x {dp_per_pass} fp64 instr",
+                     "work_note": ("sample-passes the kernels evaluated: with bounded_search = 1 (the default) "
+                                   f"{counters.get('n_pruned_queries', 0)} of "
+                                   f"{counters['n_candidate_queries'] + counters['n_local_queries']} queries stopped "
+                                   "once their partial Err proved they cannot be the argmin; their evaluated pairs "
+                                   "count, the rest do not"),
                      "peak_note": f"148 SMs x 64 fp64/clk x {sm_max:.0f} MHz (sm_max_mhz, {peak_kind})"},
         "roofline_spectral": {"bound": "hbm", "kernel": "composite + spectrum (a1-a3)",
                               "achieved": alg_bytes / (spec_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -374,8 +379,9 @@ def run_gpu(args) -> None:
         "phase_ms": {n: float(v) for n, v in zip(g.PHASES, phase_ms)},
         "work_counters": counters,
         "clocks": clocks,
-        # fused spectrum (1), 2 x scorer (team, mid and xl bucketed: 3), select (1), final (1) per call
-        "gpu_launches": 9 * args.steps * len(chunks),
+        # fused spectrum (1), candidate list (scan + scatter: 2), 2 x scorer (team, mid and xl bucketed: 3),
+        # select (select, scan, scatter: 3), final (1) per call
+        "gpu_launches": 13 * args.steps * len(chunks),
     }
     B = min(B, Bbuf)  # the sub-lines below use the resident buffer
 
@@ -550,7 +556,7 @@ def run_gpu(args) -> None:
                          "work": f"{c5['cem_sample_passes']} CEM sample-passes/step x {3 * p5.num_groups + 2} fp64 instr"},
             "work_counters": c5,
             "status_counts": {str(k): int(v) for k, v in zip(*np.unique(r5["status"], return_counts=True))},
-            "gpu_launches": 10 * args.steps,  # composite, cluster spectrum, 2 x 3 scorers, select, final
+            "gpu_launches": 14 * args.steps,  # composite, cluster spectrum, candidate list (2), 2 x 3 scorers, select (3), final
         }
         if rank == 0 and not args.no_cpu_baseline:
             line["cfg5"]["cpu_baseline"] = cpu_baseline(spec5, args.cfg5_cpu_traces, os.cpu_count() or 1,
