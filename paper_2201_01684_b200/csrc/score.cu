@@ -587,6 +587,32 @@ struct BucketView {
   }
 };
 
+#ifndef GPOEO_WIN_PREFETCH
+#define GPOEO_WIN_PREFETCH 1
+#endif
+// L2 prefetch of the window [w, w + L) (one bulk prefetch over the 16-B aligned cover; the
+// trace row ends at or before `end`): issued a pair ahead so the final pass and the next
+// pair's counting sort read L2 instead of waiting on HBM.
+__device__ __forceinline__ void prefetch_window(const float* w, int32_t L, const float* end) {
+#if GPOEO_WIN_PREFETCH
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(w) & ~(uintptr_t)15;
+  uintptr_t a1 = (reinterpret_cast<uintptr_t>(w + L) + 15) & ~(uintptr_t)15;
+  const uintptr_t lim = reinterpret_cast<uintptr_t>(end) & ~(uintptr_t)15;
+  if (a1 > lim) a1 = lim;
+  if (a1 > a0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+#endif
+}
+
+// The windows of round r of a team-kernel query (pairs r*nteams .. r*nteams + nteams - 1 read
+// windows up to one past their last pair).
+__device__ __forceinline__ void prefetch_round(const float* yt, int32_t L, int nteams, int r, int32_t npairs,
+                                               const float* end) {
+  const int64_t p0 = (int64_t)r * nteams;
+  if (p0 >= npairs) return;
+  const int64_t p1 = p0 + nteams < npairs ? p0 + nteams : npairs;  // last window index read: p1
+  prefetch_window(yt + p0 * L, (int32_t)((p1 - p0 + 1) * L), end);
+}
+
 // Real roots of s_j(y) = s_k(y) with s(y) = c - h (y - mu)^2, in coordinates z = y - m0.
 __device__ __forceinline__ void score_crossings(double muj, double cj, double hj, double muk, double ck, double hk,
                                                 double m0, double& r0, double& r1) {
@@ -1222,9 +1248,11 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
     const int32_t npairs = (a.row_n ? a.row_n[t] : a.N) / L - 1;
     const float* yt = a.y + t * a.ystride;
     double acc = 0.0;
+    const float* yend = yt + (a.row_n ? a.row_n[t] : a.N);
     int tau = 1;
     while (tau * kLpt < L) tau <<= 1;
     const int nteams = kScoreThreads / tau;
+    if (tid == 0) prefetch_round(yt, L, nteams, 0, npairs, yend);  // the first round's windows
     const int team = tid / tau;
     const int lt = tid & (tau - 1);
     // warp-uniform trip count (sub-warp teams of one warp: team0 .. team0 + 32/tau - 1)
@@ -1238,6 +1266,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
       for (int i = 0; i < trips; ++i) {
         const int pidx = team + i * nteams;
         const bool has = pidx < npairs;
+        if (tid == 0) prefetch_round(yt, L, nteams, i + 1, npairs, yend);
         const float* A = yt + (int64_t)(has ? pidx : 0) * L;
         const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
         if (has) acc += e;
@@ -1257,6 +1286,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
       for (int i = 0; i < trips; ++i) {
         const int pidx = team + i * nteams;
         const bool has = pidx < npairs;
+        if (tid == 0) prefetch_round(yt, L, nteams, i + 1, npairs, yend);
         const float* A = yt + (int64_t)(has ? pidx : 0) * L;
         const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
         if (has) acc += e;
@@ -1318,7 +1348,11 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
       BucketView bv =
           BucketView::carve(s_dyn + (size_t)warp * bucket_region_bytes(a.bucket_lcap, VS), a.bucket_lcap, VS);
       float2 range = make_float2(0.f, 0.f);
+      const float* yend = yt + (a.row_n ? a.row_n[t] : a.N);
+      if (lane == 0) prefetch_window(yt, 2 * L, yend);
       for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
+        // W_{i+2}: read by this pair's successor's final pass
+        if (lane == 0 && pidx + 2 <= npairs) prefetch_window(yt + (int64_t)(pidx + 2) * L, L, yend);
         // kBucketWarps == 1: pairs in order, so the previous final pass saw this W_i
         acc += pair_err_bucket<G, VS>(yt + (int64_t)pidx * L, L, lane, bv, a.maxit, passes, pidx != warp, range);
         __syncwarp();
