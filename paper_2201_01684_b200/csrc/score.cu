@@ -128,7 +128,11 @@ __device__ __forceinline__ void team_allreduce(double* v, int tau, int team, int
 }
 
 // CEM model of one window (identical in every lane of the team). Dead components carry
-// c = -inf, h = 0 so the assignment needs no liveness test.
+// c = -inf, h = 0 so the assignment needs no liveness test. The initial model has c = 0,
+// h = 1 for every component: the general rule then scores -(y - mu_j)^2 exactly (the product
+// by 1 and the sum with 0 are exact, so a contraction changes nothing) and its argmax with
+// ties to the lowest j is the first pass's argmin (y - mu_j)^2 on exactly rounded values (R1)
+// -- one code path for every pass.
 template <int G>
 struct Cem {
   double mu[G], c[G], h[G];
@@ -140,33 +144,19 @@ struct Cem {
     for (int j = 0; j < G; ++j) {
       mu[j] = __dadd_rn(mn, __dmul_rn((double)j + 0.5, w));
       c[j] = 0.0;
-      h[j] = 0.0;
+      h[j] = 1.0;
     }
     floor_var = __dmul_rn(__dmul_rn(1e-6, R), R);
   }
 
-  // first pass: every pi_j, var_j equal -> argmin (y - mu_j)^2 on exactly rounded values
-  __device__ __forceinline__ int assign_first(double y, double* e) const {
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const double d = __dsub_rn(y, mu[j]);
-      e[j] = __dmul_rn(d, d);
-    }
-    int best = 0;
-    double bs = e[0];
-#pragma unroll
-    for (int j = 1; j < G; ++j)
-      if (e[j] < bs) { best = j; bs = e[j]; }
-    return best;
-  }
-
-  // later passes: argmax ln pi_j - 1/2 ln var_j - (y - mu_j)^2/(2 var_j); e[j] = (y - mu_j)^2
+  // argmax_j ln pi_j - 1/2 ln var_j - (y - mu_j)^2/(2 var_j) = c_j - h_j (y - mu_j)^2, ties to
+  // the lowest j; e[j] = (y - mu_j)^2
   __device__ __forceinline__ int assign(double y, double* e) const {
     double sc[G];
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const double d = y - mu[j];
-      e[j] = d * d;
+      const double d = __dsub_rn(y, mu[j]);
+      e[j] = __dmul_rn(d, d);
       sc[j] = fma(-e[j], h[j], c[j]);
     }
     int best = 0;
@@ -175,10 +165,6 @@ struct Cem {
     for (int j = 1; j < G; ++j)
       if (sc[j] > bs) { best = j; bs = sc[j]; }
     return best;
-  }
-
-  __device__ __forceinline__ int assign(double y, int it, double* e) const {
-    return it == 1 ? assign_first(y, e) : assign(y, e);
   }
 };
 
@@ -393,33 +379,20 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
 #pragma unroll
     for (int j = 0; j < G; ++j) n[j] = 0;
     if (active) {
-      if (it == 1) {
+      // the new labels are packed afresh; "any label changed" is one compare of the words
+      uint64_t nl = 0;
 #pragma unroll 1
-        for (int u = 0; u < cnt; ++u) {
-          const double y = ys[u * kScoreThreads];
-          double e[G];
-          const int b = cem.assign_first(y, e);
-          labs |= (uint64_t)b << (4 * u);
+      for (int u = 0; u < cnt; ++u) {
+        const double y = ys[u * kScoreThreads];
+        double e[G];
+        const int b = cem.assign(y, e);
+        nl |= (uint64_t)b << (4 * u);
 #pragma unroll
-          for (int j = 0; j < G; ++j)
-            if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
-        }
-      } else {
-        // the new labels are packed afresh; "any label changed" is one compare of the words
-        uint64_t nl = 0;
-#pragma unroll 1
-        for (int u = 0; u < cnt; ++u) {
-          const double y = ys[u * kScoreThreads];
-          double e[G];
-          const int b = cem.assign(y, e);
-          nl |= (uint64_t)b << (4 * u);
-#pragma unroll
-          for (int j = 0; j < G; ++j)
-            if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
-        }
-        changed = nl != labs;
-        labs = nl;
+        for (int j = 0; j < G; ++j)
+          if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
       }
+      changed = it > 1 && nl != labs;
+      labs = nl;
     }
 #if GPOEO_TEAM_RS
     if (tau >= team_rs_min<G>() && tau <= 32) {  // warp-uniform (one query per CTA)
@@ -587,6 +560,13 @@ struct BucketView {
   }
 };
 
+#ifndef GPOEO_SORT_UNROLL
+#define GPOEO_SORT_UNROLL 4  // counting-sort loops over the window (global loads in flight per lane)
+#endif
+#ifndef GPOEO_FINAL_UNROLL
+#define GPOEO_FINAL_UNROLL 1  // final W_i / W_{i+1} pass (rolled: smaller code, measured faster than 2, 4, 8)
+#endif
+constexpr int kSortUnroll = GPOEO_SORT_UNROLL, kFinalUnroll = GPOEO_FINAL_UNROLL;
 #ifndef GPOEO_WIN_PREFETCH
 #define GPOEO_WIN_PREFETCH 1
 #endif
@@ -704,7 +684,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   auto bucket_of = [&](int s) -> int { return bucket_of_v(__ldg(A + s)); };
 #pragma unroll
   for (int b = 0; b < kBuckets; ++b) bv.lcnt[b * 32 + lane] = 0;
-#pragma unroll 4
+#pragma unroll kSortUnroll
   for (int s = lane; s < L; s += 32) {
     const int b = bucket_of(s);
     bv.lcnt[b * 32 + lane] += 1;  // own column: no race
@@ -747,7 +727,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     if (lane == 31) bv.off[kBuckets] = (uint16_t)L;
     __syncwarp();
   }
-#pragma unroll 4
+#pragma unroll kSortUnroll
   for (int s = lane; s < L; s += 32) {
     const float v = __ldg(A + s);
     const int b = bucket_of_v(v);
@@ -790,7 +770,11 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // ---- CEM passes --------------------------------------------------------------------
   Cem<G> cem;
   cem.init(mn, R);
-  if (lane < G) bv.prm[lane] = __dadd_rn(mn, __dmul_rn((double)lane + 0.5, R / (double)G));  // = cem.mu[lane]
+  if (lane < G) {  // = cem's initial (mu, c, h)
+    bv.prm[lane] = __dadd_rn(mn, __dmul_rn((double)lane + 0.5, R / (double)G));
+    bv.prm[8 + lane] = 0.0;
+    bv.prm[16 + lane] = 1.0;
+  }
   __syncwarp();
   const double delta = 1e-6 * R;
   // root slot x = lane + 32 t (t < RPL) is root (x & 1) of component pair x >> 1
@@ -825,7 +809,6 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       // the pair's parameters from the warp's table (one load each, no select chains)
       double muj = bv.prm[pj[t]], cj = bv.prm[8 + pj[t]], hj = bv.prm[16 + pj[t]];
       double muk = bv.prm[pk[t]], ck = bv.prm[8 + pk[t]], hk = bv.prm[16 + pk[t]];
-      if (it == 1) { cj = ck = 0.0; hj = hk = 1.0; }  // first pass: argmin (y - mu)^2
       if (x < 2 * P && (x & 1) == 0) score_crossings(muj, cj, hj, muk, ck, hk, mn, r0, r1);
       const double r1_left = __shfl_up_sync(FULL, r1, 1);
       r[t] = (x & 1) ? r1_left : r0;
@@ -837,9 +820,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         for (int m = 0; m < G; ++m) {
           if (m == pj[t] || m == pk[t]) continue;
           const double dm = r[t] - cem.mu[m];
-          double sm;
-          if (it == 1) sm = -dm * dm;
-          else sm = cem.c[m] == -INFINITY ? -INFINITY : cem.c[m] - cem.h[m] * dm * dm;
+          const double sm = cem.c[m] == -INFINITY ? -INFINITY : cem.c[m] - cem.h[m] * dm * dm;
           valid &= !(sm > sj + 1e-6 * (fabs(sj) + fabs(sm) + 1.0));
         }
       }
@@ -893,7 +874,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         continue;
       }
       double e[G];
-      const int lbl = cem.assign((double)bv.bmin[b], it, e);
+      const int lbl = cem.assign((double)bv.bmin[b], e);
       const double c = (double)bv.cb[b], a1 = bv.s1[b], a2 = bv.s2[b], n = (double)cnt;
 #pragma unroll
       for (int j = 0; j < G; ++j)
@@ -924,7 +905,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
             const bool ok = slot < o1;
             const double y = ok ? (double)bv.val[slot] : 0.0;
             double e[G];
-            const int lbl = cem.assign(y, it, e);
+            const int lbl = cem.assign(y, e);
             if (ok) {
 #pragma unroll
               for (int j = 0; j < G; ++j)
@@ -998,7 +979,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
           yn = __ldg(A + pn);
         }
         double e[G];
-        const int lbl = cem.assign(y, it, e);
+        const int lbl = cem.assign(y, e);
 #pragma unroll
         for (int j = 0; j < G; ++j)
           if (lbl == j) { nc[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
@@ -1059,7 +1040,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   double TA = 0.0;
   const float* B = A + L;
   float nmn = INFINITY, nmx = -INFINITY;  // range of W_{i+1}, handed to the next pair
-#pragma unroll 4
+#pragma unroll kFinalUnroll
   for (int p = lane; p < L; p += 32) {
     const float fa = __ldg(A + p), fb = __ldg(B + p);
     const double ya = (double)fa, yb = (double)fb;
@@ -1071,7 +1052,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     if (l >= G) {
       if (VS) {  // mixed bucket: the per-sample rule of the last pass gave this value's slot its label
         double e[G];
-        l = cem.assign(ya, passes, e);
+        l = cem.assign(ya, e);
       } else {
         l = bv.lab[p];
       }
@@ -1129,7 +1110,7 @@ __device__ double pair_err_warp(const float* __restrict__ A, int32_t L, int lane
     for (int s = lane; s < L; s += 32) {
       const double v = (double)__ldg(A + s);
       double e[G];
-      const int b = cem.assign(v, it, e);
+      const int b = cem.assign(v, e);
       if (it > 1) changed |= (b != lab[s]);
       lab[s] = (uint8_t)b;
 #pragma unroll
@@ -1358,7 +1339,7 @@ __global__ void __launch_bounds__(kBucketWarps * 32, MINB) score_bucket_kernel(S
         __syncwarp();
         if (stop()) { pruned = true; break; }
       }
-    } else {
+    } else if constexpr (!VS) {  // the mid launch (VS) never sees L > its region (kBucketSplitL)
       uint8_t* lab = a.lab_scratch + ((int64_t)blockIdx.x * kBucketWarps + warp) * a.lab_stride;
       for (int pidx = warp; pidx < npairs; pidx += kBucketWarps) {
         acc += pair_err_warp<G>(yt + (int64_t)pidx * L, L, lane, lab, a.maxit, passes);
