@@ -567,6 +567,9 @@ struct BucketView {
 #define GPOEO_FINAL_UNROLL 1  // final W_i / W_{i+1} pass (rolled: smaller code, measured faster than 2, 4, 8)
 #endif
 constexpr int kSortUnroll = GPOEO_SORT_UNROLL, kFinalUnroll = GPOEO_FINAL_UNROLL;
+#ifndef GPOEO_ROOT_BUCKETS
+#define GPOEO_ROOT_BUCKETS 1  // straddling buckets marked by the root lanes (1) or by a loop over the roots (0)
+#endif
 #ifndef GPOEO_WIN_PREFETCH
 #define GPOEO_WIN_PREFETCH 1
 #endif
@@ -839,6 +842,27 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     bool stq[KPL];
 #pragma unroll
     for (int q = 0; q < KPL; ++q) stq[q] = false;
+#if GPOEO_ROOT_BUCKETS
+    if constexpr (kBuckets == 32) {
+      // each root lane marks the buckets its root falls in: bucket_of_v is monotone, so a
+      // bucket b with bmin[b] - delta <= r <= bmax[b] + delta has
+      // bucket_of_v(fl32(r - delta)) <= b <= bucket_of_v(fl32(r + delta)); those few (one or
+      // two) candidates get the exact test; one OR-reduction gives every lane its bucket's flag
+      unsigned mk = 0u;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const double rr = r[t];
+        if (((vmask[t] >> lane) & 1u) && rr >= mn - delta && rr <= mx + delta) {
+          const int b0 = bucket_of_v(__double2float_rn(rr - delta));
+          const int b1 = bucket_of_v(__double2float_rn(rr + delta));
+#pragma unroll 1
+          for (int b = b0; b <= b1; ++b)
+            if (rr >= (double)bv.bmin[b] - delta && rr <= (double)bv.bmax[b] + delta) mk |= 1u << b;
+        }
+      }
+      stq[0] = (__reduce_or_sync(FULL, mk) >> lane) & 1u;
+    } else
+#endif
     {
       double lo[KPL], hi[KPL];
 #pragma unroll
