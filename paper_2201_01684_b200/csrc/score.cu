@@ -1208,6 +1208,7 @@ struct ScoreArgs {
 // strictly (the factor covers the rounding of the product and of the final division), L
 // cannot be the argmin (ties go to the smaller L only between equal Err), and the query
 // stops. The winner itself is never stopped: its partial sums stay <= its Err * npairs.
+static_assert(kBucketMinL - 1 <= kLpt * 32, "team kernel: teams of <= 32 lanes (warp-local stop decisions, no multi-warp teams)");
 __device__ __forceinline__ double bound_scale(int32_t npairs) { return (double)npairs * (1.0 + 1e-12); }
 
 // Err(L) (or +inf for a stopped query) into the query's slot; a finished query lowers its
@@ -1234,14 +1235,18 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
   __shared__ double s_team[kScoreThreads];
   __shared__ double s_red[2 * kWarps * 32];
   __shared__ double s_ys[kLpt * kScoreThreads];  // samples, [u][thread]
-  __shared__ double s_part[2][kWarps];            // bounded search: per-warp partial sums
-  __shared__ double s_bnd[2];
+  __shared__ double s_run;  // bounded search: running sum of the query's finished pair errors (any order)
+  __shared__ int s_stop;     // bounded search: the query's partial sum exceeded its trace's bound
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long total = *a.count;
   long long passes = 0;
   int buf = 0;
   for (;;) {
-    if (tid == 0) s_item = (int64_t)atomicAdd(a.cursor, 1ull);
+    if (tid == 0) {
+      s_item = (int64_t)atomicAdd(a.cursor, 1ull);
+      s_run = 0.0;  // every warp passed the previous query's last barrier
+      s_stop = 0;
+    }
     __syncthreads();
     const int64_t item = s_item;
     __syncthreads();
@@ -1262,32 +1267,31 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
     const int lt = tid & (tau - 1);
     // warp-uniform trip count (sub-warp teams of one warp: team0 .. team0 + 32/tau - 1)
     const int team0 = tau >= 32 ? team : (warp * 32) / tau;
-    bool pruned = false;
+    const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
     if (a.bound) {
-      // bounded: CTA-uniform trips; after each, the teams' partial sums (fixed order) against
-      // the trace's current bound (one barrier per trip, double-buffered)
-      const int trips = (npairs + nteams - 1) / nteams;
+      // bounded: after each trip a warp adds its teams' new pair errors to the query's running
+      // sum (shared fp64 atomics: any order is still a lower bound of the final sum, up to
+      // rounding far inside the 1e-12 factor) and compares it with the trace's current bound;
+      // no barrier, so warps never wait for each other's trips. Err itself is summed below
+      // in the fixed team order (deterministic); only the stop decision depends on timing.
       const double scale = bound_scale(npairs);
       for (int i = 0; i < trips; ++i) {
+        if (__shfl_sync(FULL, *(volatile int*)&s_stop, 0)) break;  // warp-uniform
         const int pidx = team + i * nteams;
         const bool has = pidx < npairs;
         if (tid == 0) prefetch_round(yt, L, nteams, i + 1, npairs, yend);
         const float* A = yt + (int64_t)(has ? pidx : 0) * L;
         const double e = pair_err_team<G>(A, L, tau, lt, team, lane, warp, has, a.maxit, s_red, buf, s_ys + tid, passes);
         if (has) acc += e;
-        double part = lt == 0 ? acc : 0.0;
+        double inc = (has && lt == 0) ? e : 0.0;
 #pragma unroll
-        for (int off = 16; off; off >>= 1) part += __shfl_xor_sync(FULL, part, off);
-        if (lane == 0) s_part[i & 1][warp] = part;
-        if (tid == 0) s_bnd[i & 1] = __ldcg(a.bound + t);
-        __syncthreads();
-        double tot = 0.0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) tot += s_part[i & 1][w];
-        if (tot > s_bnd[i & 1] * scale) { pruned = true; break; }  // CTA-uniform
+        for (int off = 16; off; off >>= 1) inc += __shfl_xor_sync(FULL, inc, off);
+        if (lane == 0) {
+          const double run = atomicAdd(&s_run, inc) + inc;
+          if (run > __ldcg(a.bound + t) * scale) s_stop = 1;
+        }
       }
     } else {
-      const int trips = npairs > team0 ? (npairs - team0 + nteams - 1) / nteams : 0;
       for (int i = 0; i < trips; ++i) {
         const int pidx = team + i * nteams;
         const bool has = pidx < npairs;
@@ -1308,7 +1312,7 @@ __global__ void __launch_bounds__(kScoreThreads, GPOEO_SCORE_MINB) score_team_ke
       double sum = 0.0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) sum += s_team[w];
-      write_err(a, q, pruned, sum, npairs);
+      write_err(a, q, s_stop != 0, sum, npairs);
     }
     __syncthreads();
   }
