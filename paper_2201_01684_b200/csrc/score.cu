@@ -1061,6 +1061,9 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   double w[NV];  // nA[G], SA[G], SB[G], TB ; TA separately (same order)
 #pragma unroll
   for (int i = 0; i < NV; ++i) w[i] = 0.0;
+  int32_t na[G];  // the counts in integers (ALU, not the fp64 pipe); n_j <= L < 2^16
+#pragma unroll
+  for (int j = 0; j < G; ++j) na[j] = 0;
   double TA = 0.0;
   const float* B = A + L;
   float nmn = INFINITY, nmx = -INFINITY;  // range of W_{i+1}, handed to the next pair
@@ -1083,9 +1086,22 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     }
 #pragma unroll
     for (int j = 0; j < G; ++j)
-      if (l == j) { w[j] += 1.0; w[G + j] += ya; w[2 * G + j] += yb; }
+      if (l == j) { na[j] += 1; w[G + j] += ya; w[2 * G + j] += yb; }
   }
-  xor_sum_vec<NV>(w, 32);
+  xor_sum_vec<NV - G>(w + G, 32);
+  {
+    constexpr int NPK = (G + 1) / 2;  // two counts per 32-bit word
+    unsigned pk[NPK];
+#pragma unroll
+    for (int i = 0; i < NPK; ++i) pk[i] = (unsigned)na[2 * i] | ((2 * i + 1 < G ? (unsigned)na[2 * i + 1] : 0u) << 16);
+#pragma unroll 1
+    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NPK; ++i) pk[i] += __shfl_xor_sync(FULL, pk[i], off);
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) w[j] = (double)((pk[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+  }
 #pragma unroll 1
   for (int off = 16; off; off >>= 1) {
     TA += __shfl_xor_sync(FULL, TA, off);
