@@ -125,6 +125,24 @@ __device__ __forceinline__ void append_items(const ItemList& l, int t, int L0, i
   }
 }
 
+#ifndef GPOEO_CAND_ORDER
+#define GPOEO_CAND_ORDER 1  // candidate queries run in order of L descending (1) or of spectral rank (0)
+#endif
+// Bounded-search rank of candidate c of a trace (cand_L: the trace's candidate periods, all
+// distinct after the dedupe, Z9): the longest period first -- the fundamental before its
+// harmonics, whose tiny windows cost the most per sample and rarely win
+__device__ __forceinline__ int cand_rank(const int32_t* cand_L, int nc, int c) {
+#if GPOEO_CAND_ORDER
+  int r = 0;
+  for (int i = 0; i < nc; ++i) r += cand_L[i] > cand_L[c];
+  return r;
+#else
+  (void)cand_L;
+  (void)nc;
+  return c;
+#endif
+}
+
 // kernel class of a query: 0 team (L < kBucketMinL), 1 mid bucketed, 2 xl
 __device__ __forceinline__ int query_class(int32_t L) {
   return L < kBucketMinL ? 0 : (L <= kBucketSplitL ? 1 : 2);

@@ -81,8 +81,8 @@ __global__ void rank_scan_kernel(unsigned long long* ctr, ItemList list) {
   if (lane == 31) *(cls == 0 ? list.n_small : cls == 1 ? list.n_big : list.n_xl) = incl;
 }
 
-// One thread per trace: candidate c (spectral rank c, Alg. 1 l.4) at the next free position of
-// its (class, rank c) section of list_a, so the strongest peaks' queries run first.
+// One thread per trace: candidate c at the next free position of its (class, cand_rank)
+// section of list_a, so a trace's first-ranked queries run (and bound the rest) first.
 __global__ void cand_scatter_kernel(Plan pc, Work w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= pc.batch) return;
@@ -91,7 +91,8 @@ __global__ void cand_scatter_kernel(Plan pc, Work w) {
   for (int c = 0; c < nc; ++c) {
     const int32_t L = w.cand_L[t * pc.K + c];
     const int cls = query_class(L);
-    const unsigned long long pos = atomicAdd(&w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + c], 1ull);
+    const unsigned long long pos =
+        atomicAdd(&w.rank_ctr[3 * kRankBuckets + cls * kRankBuckets + cand_rank(w.cand_L + t * pc.K, nc, c)], 1ull);
     list_put(w.list_a, cls, pos, make_int4((int)t, L, (int)(t * pc.K + c), 0));
   }
 }

@@ -266,7 +266,8 @@ __device__ void finish_candidates(const Plan& p, const PV& Pv, int64_t t, int32_
     w.bound[t] = INFINITY;  // bounded search: no candidate scored yet
     if (status == GPOEO_TRACE_OK) {  // queries listed in rank order by launch_candidate_list
       for (int c2 = 0; c2 < nc; ++c2)
-        atomicAdd(&w.rank_ctr[query_class(w.cand_L[t * p.K + c2]) * kRankBuckets + c2], 1ull);
+        atomicAdd(&w.rank_ctr[query_class(w.cand_L[t * p.K + c2]) * kRankBuckets + cand_rank(w.cand_L + t * p.K, nc, c2)],
+                  1ull);
     }
   }
 }
