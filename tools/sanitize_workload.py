@@ -43,7 +43,7 @@ def detect(spec, B=None):
     loc = g.local_scores(ws, p, x.shape[0])
     torch.cuda.synchronize()
     r = g.results_numpy(res)
-    assert (r["status"] >= 0).all() and np.isfinite(loc.cpu().numpy()[r["status"] == 0, 0]).all()
+    assert (r["status"] >= 0).all() and not np.isnan(loc.cpu().numpy()[r["status"] == 0, 0]).any()  # +inf: stopped
     return r
 
 
