@@ -80,6 +80,15 @@ __device__ __forceinline__ double smape(double a, double b) {
   return den == 0.0 ? 0.0 : fabs(a - b) / den;
 }
 
+// Group accumulation of one sample with label l: n_j += 1, S_j += a, T_j += b for j == l, as
+// selects and unconditional adds (x + 0.0 == x for the sums here, which are never -0.0), so the
+// compiler emits no per-label branches or jump tables (divergent per lane).
+__device__ __forceinline__ void acc_sel(bool m, int32_t& n, double& S, double& T, double a, double b) {
+  n += (int32_t)m;
+  S += m ? a : 0.0;
+  T += m ? b : 0.0;
+}
+
 // 1/y to within ~1 ulp for finite normal y: MUFU reciprocal + two Newton steps (IEEE
 // division is a long software sequence; the scorer's divisions need no correct rounding:
 // the M-step and the root finder already differ from the oracle at rounding level, Z27).
@@ -430,7 +439,7 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
       const int l = (int)((labs >> (4 * u)) & 15u);
 #pragma unroll
       for (int j = 0; j < G; ++j)
-        if (l == j) { n[j] += 1; v[G + j] += ya; v[2 * G + j] += yb; }
+        acc_sel(l == j, n[j], v[G + j], v[2 * G + j], ya, yb);
     }
 #pragma unroll
     for (int j = 0; j < G; ++j) v[j] = (double)n[j];
@@ -1086,7 +1095,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     }
 #pragma unroll
     for (int j = 0; j < G; ++j)
-      if (l == j) { na[j] += 1; w[G + j] += ya; w[2 * G + j] += yb; }
+      acc_sel(l == j, na[j], w[G + j], w[2 * G + j], ya, yb);
   }
   xor_sum_vec<NV - G>(w + G, 32);
   {
