@@ -27,6 +27,8 @@
 //    shared memory or global scratch).
 //  * Err(L) is the sum of per-team partial sums in team order: deterministic.
 
+#include <type_traits>
+
 #include "gpoeo_internal.cuh"
 
 namespace gpoeo {
@@ -374,7 +376,10 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
   bool active = clustered;
   Cem<G> cem;
   cem.init(mn, R);
-  uint64_t labs = 0;  // 4-bit labels of the lane's <= 16 samples
+  // the labels of the lane's <= 16 samples, LB bits each: one 32-bit word for G <= 4
+  using LabWord = typename std::conditional<(G <= 4), uint32_t, uint64_t>::type;
+  constexpr int LB = G <= 2 ? 1 : (G <= 4 ? 2 : 4);
+  LabWord labs = 0;
   int passes = 0;
   for (int it = 1; it <= maxit; ++it) {
     if (!__any_sync(FULL, active)) break;
@@ -389,13 +394,13 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
     for (int j = 0; j < G; ++j) n[j] = 0;
     if (active) {
       // the new labels are packed afresh; "any label changed" is one compare of the words
-      uint64_t nl = 0;
+      LabWord nl = 0;
 #pragma unroll 1
       for (int u = 0; u < cnt; ++u) {
         const double y = ys[u * kScoreThreads];
         double e[G];
         const int b = cem.assign(y, e);
-        nl |= (uint64_t)b << (4 * u);
+        nl |= (LabWord)b << (LB * u);
 #pragma unroll
         for (int j = 0; j < G; ++j)
           if (b == j) { n[j] += 1; v[G + j] += y; v[2 * G + j] += e[j]; }
@@ -436,7 +441,7 @@ __device__ double pair_err_team(const float* __restrict__ A, int32_t L, int tau,
       const double ya = ys[u * kScoreThreads];
       const double yb = (double)__ldg(B + lt + u * tau);
       v[3 * G] += yb;
-      const int l = (int)((labs >> (4 * u)) & 15u);
+      const int l = (int)((labs >> (LB * u)) & ((1u << LB) - 1u));
 #pragma unroll
       for (int j = 0; j < G; ++j)
         acc_sel(l == j, n[j], v[G + j], v[2 * G + j], ya, yb);
