@@ -12,11 +12,49 @@
 
 namespace gpoeo {
 
-// rank of a local query: distance from L_b, the smaller side first (L_b - 1, L_b + 1,
-// L_b - 2, ...); L_b itself is a candidate (memoised)
-__device__ __forceinline__ int local_rank(int32_t L, int32_t Lb) {
-  const int d = L - Lb;
-  const int r = d < 0 ? -2 * d - 2 : 2 * d - 1;
+#ifndef GPOEO_LOCAL_CENTER
+#define GPOEO_LOCAL_CENTER 1  // local queries ordered around the harmonic period estimate (1) or L_b (0)
+#endif
+// Where the local range's best L is most likely (this only orders the queries of the bounded
+// search; every L of the range is still scored or proved worse): N / k_b, refined by the
+// highest harmonic among the candidates -- a bin k_h ~ h k_b (|k_h - h k_b| <= h/2 + 1) puts
+// the period at h N / k_h, h times finer than the bin spacing at k_b -- if that estimate
+// lies in the range.
+__device__ __forceinline__ double local_center(const int32_t* cand_k, int nc, int64_t kb, int64_t N, int64_t lo,
+                                               int64_t hi) {
+  double c = (double)N / (double)kb;
+#if GPOEO_LOCAL_CENTER
+  int64_t hb = 1;
+  for (int q = 0; q < nc; ++q) {
+    const int64_t k = cand_k[q];
+    const int64_t h = (k + kb / 2) / kb;  // nearest multiple of k_b
+    const int64_t dev = k - h * kb;
+    if (h > hb && 2 * (dev < 0 ? -dev : dev) <= h + 2) {
+      const double e = (double)(h * N) / (double)k;
+      if (e >= (double)lo && e <= (double)(hi + 1)) {
+        hb = h;
+        c = e;
+      }
+    }
+  }
+#endif
+  return c;
+}
+
+// rank of a local query: by distance from the centre c (fractional), the nearest first; with
+// f = c - floor(c): below-side distances m + f, above-side m + 1 - f, merged (ties: below)
+__device__ __forceinline__ int local_rank(int32_t L, double c) {
+  const double fl = floor(c);
+  const double f = c - fl;
+  const int64_t Lf = (int64_t)fl;
+  int r;
+  if (L <= Lf) {
+    const int m = (int)(Lf - L);
+    r = f <= 0.5 ? 2 * m : 2 * m + 1;
+  } else {
+    const int m = (int)(L - Lf - 1);
+    r = f <= 0.5 ? 2 * m + 1 : 2 * m;
+  }
   return r < kRankBuckets - 1 ? r : kRankBuckets - 1;
 }
 
@@ -53,7 +91,7 @@ __global__ void select_kernel(Plan pc, Work w) {
   // Err(L) is the same deterministic value (same kernel class for the same L), so it is
   // copied (the oracle memoises identically). The queries are counted per (kernel class,
   // rank) here and listed in rank order by local_scatter_kernel.
-  const int32_t Lb = (int32_t)(N / kb);
+  const double ctr = local_center(w.cand_k + t * p.K, nc, kb, N, lo, hi);
   for (int64_t L = lo; L <= hi; ++L) {
     int c = -1;
     for (int q = 0; q < nc; ++q)
@@ -61,7 +99,7 @@ __global__ void select_kernel(Plan pc, Work w) {
     if (c >= 0) {
       w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
     } else {
-      atomicAdd(&w.rank_ctr[kRankCtrPhase + query_class((int32_t)L) * kRankBuckets + local_rank((int32_t)L, Lb)], 1ull);
+      atomicAdd(&w.rank_ctr[kRankCtrPhase + query_class((int32_t)L) * kRankBuckets + local_rank((int32_t)L, ctr)], 1ull);
     }
   }
 }
@@ -115,14 +153,14 @@ __global__ void local_scatter_kernel(Plan pc, Work w) {
   const int nc = w.n_cand[t];
   const int32_t lo = w.local_lo[t], hi = w.local_hi[t];
   const int64_t base = w.local_base[t];
-  const int32_t Lb = p.N / w.best_bin[t];
+  const double ctr = local_center(w.cand_k + t * p.K, nc, w.best_bin[t], p.N, lo, hi);
   for (int32_t L = lo; L <= hi; ++L) {
     bool memo = false;
     for (int q = 0; q < nc; ++q) memo |= w.cand_L[t * p.K + q] == L;
     if (memo) continue;
     const int cls = query_class(L);
     const unsigned long long pos =
-        atomicAdd(&w.rank_ctr[kRankCtrPhase + 3 * kRankBuckets + cls * kRankBuckets + local_rank(L, Lb)], 1ull);
+        atomicAdd(&w.rank_ctr[kRankCtrPhase + 3 * kRankBuckets + cls * kRankBuckets + local_rank(L, ctr)], 1ull);
     list_put(w.list_b, cls, pos, make_int4((int)t, L, (int)(base + (L - lo)), 0));
   }
 }
