@@ -106,7 +106,7 @@ Plan make_plan(const gpoeo_params* p, int64_t batch) {
 
 struct Layout {
   size_t off_y, off_status, off_ncand, off_ck, off_cL, off_cP, off_cerr, off_bb, off_llo, off_lhi, off_lbase,
-      off_ia, off_ib, off_xa, off_xb, off_lerr, off_lab, off_ctr, off_bound, total;
+      off_ia, off_ib, off_xa, off_xb, off_lerr, off_lab, off_ctr, off_bound, off_center, total;
   int32_t lab_stride;
 };
 
@@ -132,6 +132,7 @@ Layout layout(const Plan& pl) {
   L.off_lhi = take(sizeof(int32_t) * B);
   L.off_lbase = take(sizeof(int64_t) * B);
   L.off_bound = take(sizeof(double) * B);
+  L.off_center = take(sizeof(double) * B);
   L.off_ia = take(sizeof(int4) * B * K);
   L.off_ib = take(sizeof(int4) * B * ML);
   // xl arrays (L > kBucketSplitL) only when the band reaches there
@@ -161,6 +162,7 @@ Work carve(const Plan& pl, const Layout& L, void* ws) {
   w.local_hi = reinterpret_cast<int32_t*>(b + L.off_lhi);
   w.local_base = reinterpret_cast<int64_t*>(b + L.off_lbase);
   w.bound = reinterpret_cast<double*>(b + L.off_bound);
+  w.center = reinterpret_cast<double*>(b + L.off_center);
   w.rank_ctr = w.ctr + kRankCtrBase;
   w.list_a = ItemList{reinterpret_cast<int4*>(b + L.off_ia), (int64_t)pl.batch * pl.K, &w.ctr[CTR_A_SMALL],
                       &w.ctr[CTR_A_BIG], &w.ctr[CTR_CUR_A_SMALL], &w.ctr[CTR_CUR_A_BIG],

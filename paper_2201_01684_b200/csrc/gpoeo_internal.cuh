@@ -178,6 +178,7 @@ struct Work {
   int32_t* local_hi;        // [B]
   int64_t* local_base;      // [B]
   double* bound;            // [B] bounded search: the smallest Err a finished query of the trace reached
+  double* center;           // [B] bounded search: where the local range's best L most likely is (order only)
   unsigned long long* rank_ctr;  // [2 phases][2][3][kRankBuckets] rank-ordered list construction (in ctr)
   ItemList list_a;          // [B*K]   candidate queries (trace, L, out slot, -)
   ItemList list_b;          // [B*max_local] local queries

@@ -89,18 +89,97 @@ __global__ void select_kernel(Plan pc, Work w) {
   w.bound[t] = w.cand_err[t * p.K + best];
   // Alg. 2 on every L of the range, except candidates already scored in phase a4: their
   // Err(L) is the same deterministic value (same kernel class for the same L), so it is
-  // copied (the oracle memoises identically). The queries are counted per (kernel class,
-  // rank) here and listed in rank order by local_scatter_kernel.
-  const double ctr = local_center(w.cand_k + t * p.K, nc, kb, N, lo, hi);
+  // copied (the oracle memoises identically). The remaining queries are ordered around
+  // w.center[t] (refined by center_refine_kernel for wide ranges), counted per (kernel class,
+  // rank) by local_count_kernel and listed by local_scatter_kernel.
+  w.center[t] = local_center(w.cand_k + t * p.K, nc, kb, N, lo, hi);
   for (int64_t L = lo; L <= hi; ++L) {
     int c = -1;
     for (int q = 0; q < nc; ++q)
       if (w.cand_L[t * p.K + q] == (int32_t)L) c = q;
-    if (c >= 0) {
-      w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
-    } else {
-      atomicAdd(&w.rank_ctr[kRankCtrPhase + query_class((int32_t)L) * kRankBuckets + local_rank((int32_t)L, ctr)], 1ull);
+    if (c >= 0) w.local_err[base + (L - lo)] = w.cand_err[t * p.K + c];
+  }
+}
+
+#ifndef GPOEO_CENTER_REFINE
+#define GPOEO_CENTER_REFINE 1
+#endif
+constexpr int kRefineMinRange = 8;  // local ranges at least this wide get the interpolated centre
+
+// One warp per trace with a wide local range: |X_k| at k = k_b - 1, k_b, k_b + 1 by the DFT
+// definition over y (fp32, twiddles re-seeded every 64 samples), then the rectangular-window
+// bin interpolation delta = |X_{k+1}| / (|X_k| + |X_{k+1}|) (or -|X_{k-1}| / (|X_k| + |X_{k-1}|))
+// and the centre N / (k_b + delta), clipped to the range. Only the order of the bounded
+// search's queries depends on it.
+__global__ void center_refine_kernel(Plan pc, Work w) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= pc.batch) return;
+  if (w.status[t] != GPOEO_TRACE_OK) return;
+  const int32_t lo = w.local_lo[t], hi = w.local_hi[t];
+  if (hi - lo + 1 < kRefineMinRange) return;
+  const Plan p = row_plan(pc, t);
+  const int64_t N = p.N, kb = w.best_bin[t];
+  const float* yt = w.y + t * pc.ystride;
+  float re[3] = {0.f, 0.f, 0.f}, im[3] = {0.f, 0.f, 0.f};
+  for (int64_t n0 = 0; n0 < N; n0 += 64 * 32) {
+    float2 wv[3], st[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const int64_t k = kb - 1 + b;
+      const int64_t m = (k * (n0 + lane)) % N;  // exact phase of this lane's first sample
+      float sn, cs;
+      sincospif(-2.0f * (float)m / (float)N, &sn, &cs);
+      wv[b] = make_float2(cs, sn);
+      const int64_t ms = (k * 32) % N;  // per-step rotation
+      sincospif(-2.0f * (float)ms / (float)N, &sn, &cs);
+      st[b] = make_float2(cs, sn);
     }
+    const int64_t n1 = n0 + 64 * 32 < N ? n0 + 64 * 32 : N;
+    for (int64_t n = n0 + lane; n < n1; n += 32) {
+      const float v = __ldg(yt + n);
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        re[b] = fmaf(v, wv[b].x, re[b]);
+        im[b] = fmaf(v, wv[b].y, im[b]);
+        const float x = wv[b].x * st[b].x - wv[b].y * st[b].y;
+        wv[b].y = wv[b].x * st[b].y + wv[b].y * st[b].x;
+        wv[b].x = x;
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+    for (int off = 16; off; off >>= 1) {
+      re[b] += __shfl_xor_sync(0xffffffffu, re[b], off);
+      im[b] += __shfl_xor_sync(0xffffffffu, im[b], off);
+    }
+  if (lane == 0) {
+    const float a = sqrtf(re[0] * re[0] + im[0] * im[0]), m = sqrtf(re[1] * re[1] + im[1] * im[1]),
+                c = sqrtf(re[2] * re[2] + im[2] * im[2]);
+    const float den = c > a ? m + c : m + a;
+    if (den > 0.f) {
+      const double delta = c > a ? (double)(c / den) : -(double)(a / den);
+      double ctr = (double)N / ((double)kb + delta);
+      if (ctr < (double)lo) ctr = (double)lo;
+      if (ctr > (double)hi + 1.0) ctr = (double)hi + 1.0;
+      w.center[t] = ctr;
+    }
+  }
+}
+
+// One thread per trace: the local queries per (kernel class, rank around the centre).
+__global__ void local_count_kernel(Plan pc, Work w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= pc.batch) return;
+  if (w.status[t] != GPOEO_TRACE_OK) return;
+  const int nc = w.n_cand[t];
+  const int32_t lo = w.local_lo[t], hi = w.local_hi[t];
+  const double ctr = w.center[t];
+  for (int32_t L = lo; L <= hi; ++L) {
+    bool memo = false;
+    for (int q = 0; q < nc; ++q) memo |= w.cand_L[t * pc.K + q] == L;
+    if (!memo) atomicAdd(&w.rank_ctr[kRankCtrPhase + query_class(L) * kRankBuckets + local_rank(L, ctr)], 1ull);
   }
 }
 
@@ -153,7 +232,7 @@ __global__ void local_scatter_kernel(Plan pc, Work w) {
   const int nc = w.n_cand[t];
   const int32_t lo = w.local_lo[t], hi = w.local_hi[t];
   const int64_t base = w.local_base[t];
-  const double ctr = local_center(w.cand_k + t * p.K, nc, w.best_bin[t], p.N, lo, hi);
+  const double ctr = w.center[t];
   for (int32_t L = lo; L <= hi; ++L) {
     bool memo = false;
     for (int q = 0; q < nc; ++q) memo |= w.cand_L[t * p.K + q] == L;
@@ -236,6 +315,10 @@ cudaError_t launch_select(const Plan& p, Work w, cudaStream_t s) {
   if (p.batch == 0) return cudaSuccess;
   const unsigned g = (unsigned)((p.batch + 127) / 128);
   select_kernel<<<g, 128, 0, s>>>(p, w);
+#if GPOEO_CENTER_REFINE
+  center_refine_kernel<<<(unsigned)((p.batch * 32 + 255) / 256), 256, 0, s>>>(p, w);
+#endif
+  local_count_kernel<<<g, 128, 0, s>>>(p, w);
   rank_scan_kernel<<<1, 3 * 32, 0, s>>>(w.rank_ctr + kRankCtrPhase, w.list_b);
   local_scatter_kernel<<<g, 128, 0, s>>>(p, w);
   return cudaGetLastError();
