@@ -380,8 +380,8 @@ def run_gpu(args) -> None:
         "work_counters": counters,
         "clocks": clocks,
         # fused spectrum (1), candidate list (scan + scatter: 2), 2 x scorer (team, mid and xl bucketed: 3),
-        # select (select, scan, scatter: 3), final (1) per call
-        "gpu_launches": 13 * args.steps * len(chunks),
+        # select (select, centre refine, count, scan, scatter: 5), final (1) per call
+        "gpu_launches": 15 * args.steps * len(chunks),
     }
     B = min(B, Bbuf)  # the sub-lines below use the resident buffer
 
@@ -556,7 +556,7 @@ def run_gpu(args) -> None:
                          "work": f"{c5['cem_sample_passes']} CEM sample-passes/step x {3 * p5.num_groups + 2} fp64 instr"},
             "work_counters": c5,
             "status_counts": {str(k): int(v) for k, v in zip(*np.unique(r5["status"], return_counts=True))},
-            "gpu_launches": 14 * args.steps,  # composite, cluster spectrum, candidate list (2), 2 x 3 scorers, select (3), final
+            "gpu_launches": 16 * args.steps,  # composite, cluster spectrum, candidate list (2), 2 x 3 scorers, select (5), final
         }
         if rank == 0 and not args.no_cpu_baseline:
             line["cfg5"]["cpu_baseline"] = cpu_baseline(spec5, args.cfg5_cpu_traces, os.cpu_count() or 1,
