@@ -366,31 +366,49 @@ __global__ void __launch_bounds__(SpecCfg<LOGN2>::T) spectrum_kernel(Plan p, con
   const int n = n2 * C;
   const float2* z = reinterpret_cast<const float2*>(y + t * p.ystride);
 
-  // ---- load + DIF split across the cluster: a_q[j2] -------------------------------
-  float2 wq[C];  // W_C^((r q) mod C), fixed per CTA
+  // ---- load + DIF split across the cluster: a_s[j2] = (sum_r z[j2 + r n2] W_C^(r s)) W_n^(j2 s)
+  // lands in CTA s. Each CTA reads only its slice j2 in [q n2/C, (q+1) n2/C) of every block r
+  // (the trace is read once per cluster, not C times), evaluates all C outputs there and
+  // stores a_s into CTA s's buffer through DSMEM; a cluster barrier then publishes them.
+  if constexpr (C == 1) {
+    for (int j2 = threadIdx.x; j2 < n2; j2 += T) buf[j2] = __ldg(z + j2);
+    __syncthreads();
+  } else {
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // every CTA of the cluster has started: its shared memory may be written
+    float2* dst[C];
 #pragma unroll
-  for (int r = 0; r < C; ++r) {
-    float s, c;
-    sincospif(-2.0f * (float)((r * q) % C) / (float)C, &s, &c);
-    wq[r] = make_float2(c, s);
-  }
-  for (int j2 = threadIdx.x; j2 < n2; j2 += T) {
-    float2 acc;
-    if constexpr (C == 1) {
-      acc = __ldg(z + j2);
-    } else {
-      acc = make_float2(0.f, 0.f);
+    for (int r = 0; r < C; ++r) dst[r] = cluster.map_shared_rank(buf, r);
+    float2 wc[C];  // W_C^m
 #pragma unroll
-      for (int r = 0; r < C; ++r) acc = cadd(acc, cmul(__ldg(z + j2 + r * n2), wq[r]));
-      if (q) {
-        float s, c;
-        sincospif(-2.0f * (float)(j2 * q) / (float)n, &s, &c);
-        acc = cmul(acc, make_float2(c, s));
+    for (int m = 0; m < C; ++m) {
+      float sn, cs;
+      sincospif(-2.0f * (float)m / (float)C, &sn, &cs);
+      wc[m] = make_float2(cs, sn);
+    }
+    constexpr int SL = n2 / C;
+    for (int j2 = q * SL + (int)threadIdx.x; j2 < (q + 1) * SL; j2 += T) {
+      float2 zr[C];
+#pragma unroll
+      for (int r = 0; r < C; ++r) zr[r] = __ldg(z + j2 + r * n2);
+      float sn, cs;
+      sincospif(-2.0f * (float)j2 / (float)n, &sn, &cs);
+      const float2 w1 = make_float2(cs, sn);  // W_n^j2
+      float2 ws = make_float2(1.f, 0.f);       // W_n^(j2 s)
+#pragma unroll
+      for (int s2 = 0; s2 < C; ++s2) {
+        float2 acc = zr[0];
+#pragma unroll
+        for (int r = 1; r < C; ++r) acc = cadd(acc, cmul(zr[r], wc[(r * s2) % C]));
+        if (s2) {
+          ws = s2 == 1 ? w1 : cmul(ws, w1);
+          acc = cmul(acc, ws);
+        }
+        dst[s2][j2] = acc;
       }
     }
-    buf[j2] = acc;
+    cluster.sync();  // every a_s is in place
   }
-  __syncthreads();
 
   fft_inplace<LOGN2, T>(buf);
 
