@@ -108,7 +108,8 @@ typedef struct {
   int32_t cand_k[GPOEO_MAX_CANDIDATES];     /* spectral bin of each candidate               */
   int32_t cand_L[GPOEO_MAX_CANDIDATES];     /* integer period floor(N/k)                    */
   float cand_P[GPOEO_MAX_CANDIDATES];       /* |X_k|^2                                      */
-  double cand_err[GPOEO_MAX_CANDIDATES];    /* Err(L) of Alg. 2, fp64                       */
+  double cand_err[GPOEO_MAX_CANDIDATES];    /* Err(L) of Alg. 2, fp64 (+inf: stopped by the
+                                               bounded search, proved worse than the best) */
   double best_err;                          /* Err(L*), fp64                                */
 } gpoeo_detail;
 
@@ -154,8 +155,9 @@ int gpoeo_detect_periods_timed(const float* traces, int64_t batch, const gpoeo_p
  * gpoeo_detect_periods / _ex / _timed call that used it (same p and batch; enqueue it on
  * that call's stream, after it; the workspace must not have been reused since).
  *  local_err  DEVICE [batch][gpoeo_local_range_max(p)] fp64: row t holds Err(local_lo + i)
- *             at column i <= local_hi - local_lo, NaN in the rest of the row and in every
- *             row whose status is not OK. Asynchronous, allocation-free.
+ *             at column i <= local_hi - local_lo (+inf where p->bounded_search stopped the
+ *             query: that L is proved worse than the trace's winner), NaN in the rest of the
+ *             row and in every row whose status is not OK. Asynchronous, allocation-free.
  * gpoeo_local_range_max: the row length, max over the band's bins of the local-range size
  * (HOST, pure; 0 if *p is invalid). */
 int64_t gpoeo_local_range_max(const gpoeo_params* p);
