@@ -187,6 +187,31 @@ def test_similarity_exact_zero_on_periodic():
     assert (off > 0).all()
 
 
+def test_bounded_search_exact_ties_on_periodic():
+    """Exactly periodic traces: Err is exactly 0 at the period and its multiples (Z28), so the
+    bounded search's bound reaches 0; a query whose partial sum is still 0 must not stop (only a
+    strictly larger Err may), and the tie-break to the smaller L (Z17) must hold as without it."""
+    rng = np.random.default_rng(11)
+    N, F = 8192, 3
+    rows = []
+    for L0 in (37, 120, 333, 700, 1500, 2500):
+        prof = np.round(rng.uniform(0, 100, (F, L0)))
+        rows.append(np.tile(prof, (1, N // L0 + 1))[:, :N].astype(np.float32))
+    x = np.stack(rows)
+    p1 = g.default_params(N, F, min_period=10, max_period=N // 2)
+    p0 = g.default_params(N, F, min_period=10, max_period=N // 2, bounded_search=0)
+    r1, d1, l1, _ = _detect(x, p1)
+    r0, d0, l0, _ = _detect(x, p0)
+    assert r1.tobytes() == r0.tobytes()
+    ods = O.detect_batch(x, O.Params(N, F, min_period=10, max_period=N // 2))
+    for i, od in enumerate(ods):
+        assert r1[i]["status"] == od.status == 0 and r1[i]["period"] == od.period, (i, r1[i], od.period)
+        assert (d1[i]["best_err"] == 0.0) == (od.error == 0.0), (i, d1[i]["best_err"], od.error)
+    # every local L whose exhaustive Err is 0 finished with 0 (never stopped)
+    zero = l0 == 0.0
+    assert (l1[zero] == 0.0).all()
+
+
 def test_detect_config1():
     x = tg.generate_host(tg.CFG1)
     got = _detect(x, g.params_for(tg.CFG1))
