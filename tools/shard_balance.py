@@ -1,9 +1,17 @@
 #!/usr/bin/env python
 """Profiling helper: shard-to-shard work imbalance of config 4 (8 contiguous shards of S traces,
 each timed with CUDA events on one GPU): python tools/shard_balance.py 12500"""
-import sys, json, torch, numpy as np
-sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
-import paper_2201_01684_b200 as g, tracegen as tg
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2201_01684_b200 as g  # noqa: E402
+import tracegen as tg  # noqa: E402
 spec = tg.CFG4
 W, S = 8, int(sys.argv[1]) if len(sys.argv) > 1 else 12500
 p = g.params_for(spec)
