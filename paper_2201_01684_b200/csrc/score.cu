@@ -584,6 +584,9 @@ constexpr int kSortUnroll = GPOEO_SORT_UNROLL, kFinalUnroll = GPOEO_FINAL_UNROLL
 #ifndef GPOEO_ROOT_BUCKETS
 #define GPOEO_ROOT_BUCKETS 1  // straddling buckets marked by the root lanes (1) or by a loop over the roots (0)
 #endif
+#ifndef GPOEO_FINAL_FROM_CEM
+#define GPOEO_FINAL_FROM_CEM 1  // bucketed final pass: W_i's groups from the last CEM pass
+#endif
 #ifndef GPOEO_WIN_PREFETCH
 #define GPOEO_WIN_PREFETCH 1
 #endif
@@ -810,6 +813,10 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
         ++cntp;
       }
   }
+#if GPOEO_FINAL_FROM_CEM
+  double sa_last[G];  // per-lane W_i group sums of the pass that turned out to be the last
+  int na_last[G];
+#endif
   int passes = 0;
 #pragma unroll 1
   for (int it = 1; it <= maxit; ++it) {
@@ -1040,6 +1047,13 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     }  // VS
     __syncwarp();
     passes = it;
+#if GPOEO_FINAL_FROM_CEM
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      sa_last[j] = v[G + j];
+      na_last[j] = nc[j];
+    }
+#endif
 #if GPOEO_BUCKET_RS
     // the last pass needs no sums (the final pass below recomputes the groups' statistics)
     bool act = true;
@@ -1072,6 +1086,80 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
   // ---- final groups on W_i and the same index sets on W_{i+1} (position order with
   // coalesced loads; the same loop for both windows, Z28). A sample's final label is its
   // bucket's state, or its own label when the bucket is mixed. -------------------------
+#if GPOEO_FINAL_FROM_CEM
+  // W_i's groups come from the last CEM pass (its labels are the final ones): n_j, S_j reduced
+  // here; the final pass reads W_i only for the labels by position and sums W_{i+1} by them.
+  // Z28 (identical windows -> e_i = 0 exactly) is kept by an exact test: if W_{i+1} equals W_i
+  // bit for bit, RelPrev_j = RelBack_j for every j and e_i = 0.
+  double w[NV];  // nA[G], SA[G], SB[G], TB
+#pragma unroll
+  for (int i = 0; i < NV; ++i) w[i] = 0.0;
+  const float* B = A + L;
+  float nmn = INFINITY, nmx = -INFINITY;  // range of W_{i+1}, handed to the next pair
+  bool same = true;
+#pragma unroll kFinalUnroll
+  for (int p = lane; p < L; p += 32) {
+    const float fa = __ldg(A + p), fb = __ldg(B + p);
+    const double yb = (double)fb;
+    same &= __float_as_uint(fa) == __float_as_uint(fb);
+    nmn = fminf(nmn, fb);
+    nmx = fmaxf(nmx, fb);
+    w[3 * G] += yb;
+    int l = bv.blab[bucket_of_v(fa)];
+    if (l >= G) {
+      if (VS) {  // mixed bucket: the per-sample rule of the last pass gave this value's slot its label
+        double e[G];
+        l = cem.assign((double)fa, e);
+      } else {
+        l = bv.lab[p];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) w[2 * G + j] += l == j ? yb : 0.0;  // selects: no per-label branches
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    w[G + j] = sa_last[j];
+    w[j] = (double)na_last[j];
+  }
+  xor_sum_vec<NV - G>(w + G, 32);  // SA (last pass), SB, TB
+  {
+    constexpr int NPK = (G + 1) / 2;  // the counts two per 32-bit word
+    unsigned pk[NPK];
+#pragma unroll
+    for (int i = 0; i < NPK; ++i)
+      pk[i] = (unsigned)na_last[2 * i] | ((2 * i + 1 < G ? (unsigned)na_last[2 * i + 1] : 0u) << 16);
+#pragma unroll 1
+    for (int off = 16; off; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NPK; ++i) pk[i] += __shfl_xor_sync(FULL, pk[i], off);
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) w[j] = (double)((pk[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+  }
+  double TA = 0.0;
+#pragma unroll
+  for (int j = 0; j < G; ++j) TA += w[G + j];  // every sample has a label
+  const bool identical = __all_sync(FULL, same);
+#pragma unroll 1
+  for (int off = 16; off; off >>= 1) {
+    nmn = fminf(nmn, __shfl_xor_sync(FULL, nmn, off));
+    nmx = fmaxf(nmx, __shfl_xor_sync(FULL, nmx, off));
+  }
+  range = make_float2(nmn, nmx);
+  if (lane == 0) passes_out += (long long)(passes + 1) * L;
+  if (identical) {
+    GPOEO_TICK(11, tk);
+    return 0.0;
+  }
+  const double mA = TA / (double)L, mB = w[3 * G] / (double)L;
+  double num = 0.0;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    if (w[j] == 0.0) continue;
+    num += w[j] * smape(w[G + j] / w[j] - mA, w[2 * G + j] / w[j] - mB);
+  }
+#else
   double w[NV];  // nA[G], SA[G], SB[G], TB ; TA separately (same order)
 #pragma unroll
   for (int i = 0; i < NV; ++i) w[i] = 0.0;
@@ -1131,6 +1219,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
     if (w[j] == 0.0) continue;
     num += w[j] * smape(w[G + j] / w[j] - mA, w[2 * G + j] / w[j] - mB);
   }
+#endif
   GPOEO_TICK(11, tk);
   return num / (double)L;
 }
