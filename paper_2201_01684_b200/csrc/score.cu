@@ -82,6 +82,16 @@ __device__ __forceinline__ double smape(double a, double b) {
   return den == 0.0 ? 0.0 : fabs(a - b) / den;
 }
 
+// w[k] for a runtime k < G without dynamic register indexing (a select chain)
+template <int G>
+__device__ __forceinline__ double pick(const double* w, int k) {
+  double r = w[0];
+#pragma unroll
+  for (int i = 1; i < G; ++i)
+    if (i == k) r = w[i];
+  return r;
+}
+
 // Group accumulation of one sample with label l: n_j += 1, S_j += a, T_j += b for j == l, as
 // selects and unconditional adds (x + 0.0 == x for the sums here, which are never -0.0), so the
 // compiler emits no per-label branches or jump tables (divergent per lane).
@@ -587,6 +597,9 @@ constexpr int kSortUnroll = GPOEO_SORT_UNROLL, kFinalUnroll = GPOEO_FINAL_UNROLL
 #ifndef GPOEO_FINAL_FROM_CEM
 #define GPOEO_FINAL_FROM_CEM 1  // bucketed final pass: W_i's groups from the last CEM pass
 #endif
+#ifndef GPOEO_CLASSIFY_SEL
+#define GPOEO_CLASSIFY_SEL 1  // whole-bucket sums computed once and added by selects
+#endif
 #ifndef GPOEO_WIN_PREFETCH
 #define GPOEO_WIN_PREFETCH 1
 #endif
@@ -921,6 +934,20 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
       double e[G];
       const int lbl = cem.assign((double)bv.bmin[b], e);
       const double c = (double)bv.cb[b], a1 = bv.s1[b], a2 = bv.s2[b], n = (double)cnt;
+#if GPOEO_CLASSIFY_SEL
+      {  // the bucket's sums once, with the winner's mu picked; added by selects (lanes = buckets
+         // with different labels would otherwise run every label's branch in turn)
+        const double dc = c - pick<G>(cem.mu, lbl);
+        const double S = n * c + a1, Q = a2 + dc * (2.0 * a1 + n * dc);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const bool m = lbl == j;
+          nc[j] += m ? cnt : 0;
+          v[G + j] += m ? S : 0.0;
+          v[2 * G + j] += m ? Q : 0.0;
+        }
+      }
+#else
 #pragma unroll
       for (int j = 0; j < G; ++j)
         if (lbl == j) {
@@ -929,6 +956,7 @@ __device__ double pair_err_bucket(const float* __restrict__ A, int32_t L, int la
           v[G + j] += n * c + a1;
           v[2 * G + j] += a2 + dc * (2.0 * a1 + n * dc);
         }
+#endif
       changed |= (int)(bv.blab[b] != lbl);  // 0xFF (mixed) -> l changes some member
       bv.blab[b] = (uint8_t)lbl;
     }
