@@ -241,6 +241,32 @@ def test_detect_config5_first16():
     _check(x, O.params_for(spec, dft_band_only=True), _detect(x, g.params_for(spec)), "cfg5")
 
 
+@pytest.mark.slow
+def test_full_size_config5_sampled():
+    """BASELINE.json config 5 at full size, in the launch configuration bench.py times (one call
+    over 10^4 traces x 3 x 2^18 resident in HBM, bounded search on); 16 traces spread over the
+    batch checked against the oracle one by one (every decision, every candidate and local
+    score, stopped queries validated)."""
+    spec = tg.CFG5
+    B = spec.batch
+    x = torch.empty((B, spec.n_features * spec.n_samples), dtype=torch.float32, device="cuda")
+    tg.generate_device(spec, x)
+    p = g.params_for(spec)
+    res, det, ws = g.detect_periods(x, p, detail=True)
+    torch.cuda.synchronize()
+    del x
+    rng = np.random.default_rng(55)
+    idx = sorted(set([0, B - 1] + rng.choice(np.arange(1, B - 1), 14, replace=False).tolist()))
+    ti = torch.as_tensor(idx, device="cuda")
+    loc = g.local_scores(ws, p, B)[ti].cpu().numpy()
+    r = g.results_numpy(res)[idx]
+    d = g.detail_numpy(det)[idx]
+    xs = np.stack([tg.generate_host(spec, i, 1)[0] for i in idx])
+    _check(xs, O.params_for(spec, dft_band_only=True), (r, d, loc), "cfg5-full")
+    allr = g.results_numpy(res)
+    assert (allr["status"] == 0).all()
+
+
 def test_edge_cases_statuses_and_small_n():
     N = 64
     rng = np.random.default_rng(1)
